@@ -1,0 +1,188 @@
+"""CPU oracle for arXiv 2309.03308's hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` legs may import this package.  The product path
+(``paper_2309_03308_b200``) never imports it and shares no code with it.
+
+Thin ctypes wrapper over ``corr_oracle.c`` (plain C, fp64 reductions, fp32
+KSG distances, brute force; see that file's header for the paper passages each
+function follows).  ``build()`` compiles it with gcc; ``build()`` is also called
+by ``__graft_entry__.build()`` (building the checker is not using it).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "corr_oracle.c")
+_LIB = os.path.join(_HERE, "libcorr_oracle.so")
+_lib = None
+
+F32P = ctypes.POINTER(ctypes.c_float)
+F64P = ctypes.POINTER(ctypes.c_double)
+I32P = ctypes.POINTER(ctypes.c_int32)
+I64P = ctypes.POINTER(ctypes.c_int64)
+
+
+class Box(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("x0", "y0", "z0", "x1", "y1", "z1")]
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+               "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        L.oracle_ppmcc.restype = ctypes.c_double
+        L.oracle_ppmcc.argtypes = [F32P, F32P, ctypes.c_int]
+        L.oracle_digamma_int.restype = ctypes.c_double
+        L.oracle_digamma_int.argtypes = [ctypes.c_int]
+        L.oracle_knn.restype = None
+        L.oracle_knn.argtypes = [F32P, F32P, ctypes.c_int, ctypes.c_int, F32P, I32P, I32P]
+        L.oracle_ksg.restype = ctypes.c_double
+        L.oracle_ksg.argtypes = [F32P, F32P, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.oracle_eval_pairs.restype = None
+        L.oracle_eval_pairs.argtypes = [F32P, F32P, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_int, I64P, I64P, ctypes.c_int64, F64P]
+        L.oracle_knn_pairs.restype = None
+        L.oracle_knn_pairs.argtypes = [F32P, F32P, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                       I64P, I64P, ctypes.c_int64, F32P, I32P, I32P]
+        L.oracle_mix64.restype = ctypes.c_uint64
+        L.oracle_mix64.argtypes = [ctypes.c_uint64]
+        L.oracle_pair_key.restype = ctypes.c_uint64
+        L.oracle_pair_key.argtypes = [ctypes.c_uint64, ctypes.POINTER(Box), ctypes.POINTER(Box)]
+        L.oracle_sample.restype = None
+        L.oracle_sample.argtypes = [ctypes.c_uint64, ctypes.POINTER(Box), ctypes.POINTER(Box),
+                                    ctypes.c_int64, ctypes.c_int, ctypes.c_int, I64P, I64P]
+        L.oracle_region_max.restype = None
+        L.oracle_region_max.argtypes = [F32P, F32P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(Box), ctypes.POINTER(Box), ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_uint64, F64P, I64P]
+        _lib = L
+    return _lib
+
+
+# measure codes (same values as include/corr.h, restated: the oracle shares no header)
+PEARSON = 0
+KSG = 1
+F_KSG_PLUS1 = 1 << 8
+F_ABS = 1 << 9
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def ppmcc(x, y) -> float:
+    x, y = _f32(x), _f32(y)
+    assert x.shape == y.shape
+    return lib().oracle_ppmcc(_p(x, F32P), _p(y, F32P), x.size)
+
+
+def digamma_int(m: int) -> float:
+    return lib().oracle_digamma_int(int(m))
+
+
+def knn(x, y, k: int) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    x, y = _f32(x), _f32(y)
+    n = x.size
+    eps = np.empty(n, np.float32)
+    nx = np.empty(n, np.int32)
+    ny = np.empty(n, np.int32)
+    lib().oracle_knn(_p(x, F32P), _p(y, F32P), n, int(k), _p(eps, F32P), _p(nx, I32P), _p(ny, I32P))
+    return eps, nx, ny
+
+
+def ksg(x, y, k: int, plus1: bool = False) -> float:
+    x, y = _f32(x), _f32(y)
+    return lib().oracle_ksg(_p(x, F32P), _p(y, F32P), x.size, int(k), int(bool(plus1)))
+
+
+def _field(values) -> np.ndarray:
+    """[members, P] float32 contiguous."""
+    return _f32(values.cpu().numpy() if hasattr(values, "cpu") else values)
+
+
+def eval_pairs(fa, fb, measure: int, k: int, idxA, idxB) -> np.ndarray:
+    fa = _field(fa)
+    fbn = None if fb is None else _field(fb)
+    n, P = fa.shape
+    a = np.ascontiguousarray(np.asarray(idxA, np.int64))
+    b = np.ascontiguousarray(np.asarray(idxB, np.int64))
+    out = np.empty(a.size, np.float64)
+    lib().oracle_eval_pairs(_p(fa, F32P), None if fbn is None else _p(fbn, F32P), P, n, measure,
+                            int(k), _p(a, I64P), _p(b, I64P), a.size, _p(out, F64P))
+    return out
+
+
+def knn_pairs(fa, fb, k: int, idxA, idxB):
+    fa = _field(fa)
+    fbn = None if fb is None else _field(fb)
+    n, P = fa.shape
+    a = np.ascontiguousarray(np.asarray(idxA, np.int64))
+    b = np.ascontiguousarray(np.asarray(idxB, np.int64))
+    eps = np.empty((a.size, n), np.float32)
+    nx = np.empty((a.size, n), np.int32)
+    ny = np.empty((a.size, n), np.int32)
+    lib().oracle_knn_pairs(_p(fa, F32P), None if fbn is None else _p(fbn, F32P), P, n, int(k),
+                           _p(a, I64P), _p(b, I64P), a.size, _p(eps, F32P), _p(nx, I32P),
+                           _p(ny, I32P))
+    return eps, nx, ny
+
+
+def mix64(z: int) -> int:
+    return int(lib().oracle_mix64(ctypes.c_uint64(z & 0xFFFFFFFFFFFFFFFF)))
+
+
+def _box(b: Sequence[int]) -> Box:
+    return Box(*[int(v) for v in b])
+
+
+def pair_key(seed: int, A, B) -> int:
+    a, b = _box(A), _box(B)
+    return int(lib().oracle_pair_key(ctypes.c_uint64(seed), ctypes.byref(a), ctypes.byref(b)))
+
+
+def sample(seed: int, A, B, s: int, nx: int, ny: int) -> Tuple[int, int]:
+    a, b = _box(A), _box(B)
+    pa, pb = ctypes.c_int64(), ctypes.c_int64()
+    lib().oracle_sample(ctypes.c_uint64(seed), ctypes.byref(a), ctypes.byref(b), int(s), nx, ny,
+                        ctypes.byref(pa), ctypes.byref(pb))
+    return pa.value, pb.value
+
+
+def region_max(fa, fb, dims, measure: int, k: int, regA, regB, samples: int, seed: int):
+    """Returns (out_max float64 [R], out_argmax int64 [R, 2])."""
+    nx, ny, nz = dims
+    fa = _field(fa)
+    fbn = None if fb is None else _field(fb)
+    n, P = fa.shape
+    assert P == nx * ny * nz
+    R = len(regA)
+    A = (Box * R)(*[_box(b) for b in regA])
+    B = (Box * R)(*[_box(b) for b in regB])
+    out = np.empty(R, np.float64)
+    arg = np.empty((R, 2), np.int64)
+    lib().oracle_region_max(_p(fa, F32P), None if fbn is None else _p(fbn, F32P), nx, ny, nz, n,
+                            measure, int(k), A, B, R, int(samples), ctypes.c_uint64(seed),
+                            _p(out, F64P), _p(arg, I64P))
+    return out, arg
