@@ -1,0 +1,135 @@
+/*
+ * corr.h -- C ABI of libcorr.so, the B200 (sm_100a) hot path of arXiv 2309.03308
+ * ("Adaptive Sampling of 3D Spatial Correlations for Focus+Context Visualization").
+ *
+ * The three calls follow the paper's problem statement:
+ *   - an ensemble of E members on an X x Y x Z grid           (§3)
+ *   - point-to-point correlation of two grid points' member series, Pearson
+ *     (§3.2) or the Kraskov k-NN MI estimator (Eq. 2)
+ *   - the region-pair indicator = maximum of the point-pair correlations of two
+ *     bricks (§3), sampled uniformly at random (§3.1)
+ *     or exhaustively (§5.4, "all point-to-point pairs").
+ * Readings of ambiguous passages are DESIGN.md's ledger R1..R17.
+ *
+ * Conventions (all calls):
+ *   - plain C types only; no exceptions cross the ABI; every call returns a status
+ *     (CORR_OK or a negative CORR_E_*) and sets a thread-local message readable
+ *     with corr_last_error().
+ *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).  Compute calls
+ *     are asynchronous on that stream; device buffers passed in must stay valid
+ *     until the stream reaches the call.
+ *   - point index p = (z*ny + y)*nx + x (x fastest), int64.
+ *   - the library never falls back to the CPU: with no usable CUDA device every call
+ *     returns CORR_E_CUDA.
+ */
+#ifndef CORR_H_
+#define CORR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Opaque ensemble field, immutable after creation (so concurrent calls on different
+ * streams are safe).  Owns all derived device buffers (member-contiguous rows,
+ * standardised rows, tf32 split planes, sorted rows, constant-series flags). */
+typedef struct corr_field corr_field;
+
+/* Half-open grid-index box [x0,x1) x [y0,y1) x [z0,z1): a brick. */
+typedef struct {
+  int32_t x0, y0, z0, x1, y1, z1;
+} corr_box;
+
+/* `measure` = kind in the low byte, OR-ed with flags. */
+enum { CORR_PEARSON = 0, CORR_KSG = 1 };
+enum {
+  CORR_F_KSG_PLUS1 = 1 << 8, /* KSG with psi(n_x+1), psi(n_y+1) (Kraskov alg. 1; reading R1) */
+  CORR_F_ABS = 1 << 9        /* region max of |value| (reading R11)           */
+};
+enum { CORR_OK = 0, CORR_E_INVAL = -1, CORR_E_RANGE = -2, CORR_E_NOMEM = -3, CORR_E_CUDA = -4 };
+
+/* corr_field_create -- ingest one variable of an ensemble.
+ *   values   : float32 [members][nz][ny][nx] (the paper's/SPEC's file order),
+ *              host or device pointer (detected); copied, caller keeps ownership.
+ *   nx,ny,nz : grid dims >= 1;  members (n) >= 2.
+ *   device   : CUDA ordinal the field lives on; the call makes it current.
+ * Builds, on `device`: member-contiguous rows F[P][n_pad] (n_pad = ceil(n/8)*8),
+ * fp64-standardised rows Z, their tf32 split (Z_hi, Z_lo), per-row sorted copies and
+ * argsort, constant-series flags.  Synchronises `cuda_stream` (it validates input).
+ * Errors: CORR_E_INVAL (bad dims, non-finite value), CORR_E_NOMEM, CORR_E_CUDA.
+ * On success *out owns the field; release with corr_field_destroy. */
+int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, int32_t members,
+                      int32_t device, void* cuda_stream, corr_field** out);
+
+/* Frees the field's device memory (device-synchronising).  NULL is a no-op. */
+int corr_field_destroy(corr_field* f);
+
+/* Field geometry: any output pointer may be NULL. */
+int corr_field_info(const corr_field* f, int32_t* nx, int32_t* ny, int32_t* nz,
+                    int32_t* members, int32_t* device);
+
+/* corr_eval_pairs -- batched point-pair correlation ("compute
+ * correlations for multiple feature vectors simultaneously").
+ *   fa, fb   : fields; fb == NULL means fb = fa (one variable).  fb must match fa's
+ *              dims, members and device.
+ *   measure  : CORR_PEARSON or CORR_KSG, | flags.
+ *   k        : KSG neighbour order, 1 <= k <= n-1; k == 0 selects the paper's
+ *              ceil(3n/100) clamped to [1, n-1].  Ignored for Pearson.
+ *              KSG needs n >= 4.
+ *   idxA,idxB: DEVICE int64 [npairs] point indices into fa / fb.
+ *   out      : DEVICE float32 [npairs]; out[i] = corr(fa[idxA[i]], fb[idxB[i]]).
+ * Degenerate pairs are not errors: a constant series, or psi(0) in the
+ * verbatim KSG form, gives NaN (reading R10).  Pearson is clamped to [-1, 1].
+ * Out-of-range indices are detected on the device: the pair gets NaN and the next
+ * corr_check() on the stream returns CORR_E_RANGE.
+ * Errors (immediate): CORR_E_INVAL, CORR_E_CUDA. */
+int corr_eval_pairs(const corr_field* fa, const corr_field* fb, int32_t measure, int32_t k,
+                    const int64_t* idxA, const int64_t* idxB, int64_t npairs, float* out,
+                    void* cuda_stream);
+
+/* corr_region_max -- per region pair, the maximum point-pair correlation between
+ * the two bricks and its argmax.
+ *   regionA, regionB : HOST arrays [nregion_pairs] of boxes (A in fa, B in fb).
+ *   samples > 0      : evaluate `samples` uniformly random point pairs per region pair
+ *                       drawn by the counter-based sampler of reading
+ *                      R15, keyed by (seed, box A, box B) -- independent of the region
+ *                      pair's position in the list, so any sharding gives identical
+ *                      results.  Ties -> lowest sample index s.
+ *   samples == 0     : every one of the |A|*|B| pairs (exhaustive).  Ties ->
+ *                      lowest q = a_local*|B| + b_local (local index x fastest in a box).
+ *                      Pearson uses the tcgen05 split-TF32 block GEMM with a fused max.
+ *   out_max          : DEVICE float32 [R]; NaN if every evaluated value was NaN.
+ *   out_argmax       : DEVICE int64 [R][2] = (point in A, point in B), (-1,-1) if none.
+ * NaN values are skipped.  With one field (fb == NULL) the self pair (a, a) is skipped
+ * (PAPER.md:299).  CORR_F_ABS maximises |value|.  Requires samples < 2^32 and
+ * |A|*|B| < 2^32 for the exhaustive mode.
+ * Errors: CORR_E_INVAL (empty box, bad measure/k), CORR_E_RANGE (box outside the grid),
+ * CORR_E_NOMEM, CORR_E_CUDA. */
+int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure, int32_t k,
+                    const corr_box* regionA, const corr_box* regionB, int64_t nregion_pairs,
+                    int64_t samples, uint64_t seed, float* out_max, int64_t* out_argmax,
+                    void* cuda_stream);
+
+/* corr_ksg_debug -- diagnostic dump of the KSG intermediates for the bit-exact parity
+ * checks: for pair i and member e (original member order),
+ *   eps[i*n + e] = Chebyshev distance to the k-th nearest neighbour (fp32),
+ *   nx[i*n + e], ny[i*n + e] = strict marginal counts (int32).
+ * idxA/idxB/eps/nx/ny are DEVICE pointers.  Same errors as corr_eval_pairs. */
+int corr_ksg_debug(const corr_field* fa, const corr_field* fb, int32_t k, const int64_t* idxA,
+                   const int64_t* idxB, int64_t npairs, float* eps, int32_t* nx, int32_t* ny,
+                   void* cuda_stream);
+
+/* corr_check -- synchronises `cuda_stream`; returns CORR_E_RANGE (and clears the flag)
+ * if an earlier call on `f`'s device saw an out-of-range point index, CORR_E_CUDA on a
+ * CUDA error, else CORR_OK. */
+int corr_check(const corr_field* f, void* cuda_stream);
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char* corr_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CORR_H_ */

@@ -1,0 +1,374 @@
+// api.cu -- the C ABI of libcorr.so (include/corr.h): validation, field handles,
+// stream plumbing and dispatch to the hot-path kernels.  No CPU fallback: every
+// computation runs in the kernels of field.cu / ksg.cu / pearson.cu /
+// pearson_gemm.cu; without a usable CUDA device calls return CORR_E_CUDA.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "sampler.cuh"
+
+using namespace corr;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, const char* detail = nullptr) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), fmt, detail ? detail : "");
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+  g_last_error = buf;
+  return CORR_E_CUDA;
+}
+
+// Makes `device` current for the scope of a call and restores the caller's device.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != device) err = cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void free_field(corr_field* f) {
+  if (!f) return;
+  cudaFree(f->F);
+  cudaFree(f->Z);
+  cudaFree(f->Zhi);
+  cudaFree(f->Zlo);
+  cudaFree(f->S);
+  cudaFree(f->perm);
+  cudaFree(f->cflag);
+  cudaFree(f->psi);
+  cudaFree(f->err);
+  cudaFree(f->tmaps);
+  delete f;
+}
+
+// psi(m) = -gamma + sum_{t<m} 1/t at the integers m = 0..n+1 (psi(0) = NaN): the KSG
+// arguments are integers, so the exact harmonic form replaces the paper's Lanczos
+// approximation (reading R17).
+std::vector<double> digamma_table(int n) {
+  std::vector<double> t((size_t)n + 2);
+  const double gamma = 0.57721566490153286060651209008240243;
+  t[0] = NAN;
+  double h = 0.0;
+  for (int m = 1; m <= n + 1; ++m) {
+    t[m] = h - gamma;
+    h += 1.0 / (double)m;
+  }
+  return t;
+}
+
+int check_pair_fields(const corr_field* fa, const corr_field*& fb) {
+  if (!fa) return fail(CORR_E_INVAL, "field is NULL");
+  if (!fb) fb = fa;
+  if (fb->nx != fa->nx || fb->ny != fa->ny || fb->nz != fa->nz || fb->n != fa->n || fb->device != fa->device)
+    return fail(CORR_E_INVAL, "fa and fb differ in dims, members or device");
+  return CORR_OK;
+}
+
+int resolve_k(const corr_field* f, int32_t measure, int32_t& k) {
+  const int kind = measure & 0xFF;
+  if (kind != CORR_PEARSON && kind != CORR_KSG) return fail(CORR_E_INVAL, "unknown measure kind");
+  if (measure & ~(0xFF | CORR_F_KSG_PLUS1 | CORR_F_ABS)) return fail(CORR_E_INVAL, "unknown measure flags");
+  if (kind == CORR_PEARSON) {
+    k = 0;
+    return CORR_OK;
+  }
+  const int n = f->n;
+  if (n < 4) return fail(CORR_E_INVAL, "KSG needs at least 4 members (SPEC.md:184)");
+  if (k == 0) {  // k = ceil(3n/100), clamped to [1, n-1]
+    k = (3 * n + 99) / 100;
+    if (k < 1) k = 1;
+    if (k > n - 1) k = n - 1;
+  }
+  if (k < 1 || k > n - 1) return fail(CORR_E_INVAL, "k must be in [1, n-1]");
+  return CORR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* corr_last_error(void) { return g_last_error.c_str(); }
+
+int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t device,
+                      void* cuda_stream, corr_field** out) {
+  if (!out) return fail(CORR_E_INVAL, "out is NULL");
+  *out = nullptr;
+  if (!values) return fail(CORR_E_INVAL, "values is NULL");
+  if (nx < 1 || ny < 1 || nz < 1) return fail(CORR_E_INVAL, "grid dims must be >= 1");
+  if (members < 2) return fail(CORR_E_INVAL, "members must be >= 2 (SPEC.md:34)");
+  if (members > 8192) return fail(CORR_E_INVAL, "members > 8192 not supported");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return cuda_fail(e == cudaSuccess ? cudaErrorNoDevice : e, "corr_field_create");
+  if (device < 0 || device >= ndev) return fail(CORR_E_INVAL, "device ordinal out of range");
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+
+  corr_field* f = new corr_field();
+  memset(f, 0, sizeof(*f));
+  f->device = device;
+  f->nx = nx; f->ny = ny; f->nz = nz;
+  f->n = members;
+  f->n_pad = (members + 7) / 8 * 8;
+  f->P = (int64_t)nx * ny * nz;
+  const size_t row_elems = (size_t)f->P * f->n_pad;
+
+  auto alloc = [&](void** p, size_t bytes) -> bool {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  };
+  if (!alloc((void**)&f->F, row_elems * 4) || !alloc((void**)&f->Z, row_elems * 4) ||
+      !alloc((void**)&f->Zhi, row_elems * 4) || !alloc((void**)&f->Zlo, row_elems * 4) ||
+      !alloc((void**)&f->S, row_elems * 4) || !alloc((void**)&f->perm, row_elems * 2) ||
+      !alloc((void**)&f->cflag, (size_t)f->P) || !alloc((void**)&f->psi, ((size_t)members + 2) * 8) ||
+      !alloc((void**)&f->err, sizeof(int))) {
+    free_field(f);
+    return fail(CORR_E_NOMEM, "device allocation failed for the field");
+  }
+  const std::vector<double> psi = digamma_table(members);
+  e = cudaMemcpyAsync(f->psi, psi.data(), psi.size() * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(f->err, 0, sizeof(int), st);
+
+  // values: device pointer on `device` -> used in place; otherwise staged through HBM
+  const float* dvalues = values;
+  float* staging = nullptr;
+  cudaPointerAttributes attr;
+  memset(&attr, 0, sizeof(attr));
+  cudaError_t pe = cudaPointerGetAttributes(&attr, values);
+  if (pe != cudaSuccess) cudaGetLastError();
+  const bool on_device = pe == cudaSuccess &&
+                         (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
+                         attr.device == device;
+  if (e == cudaSuccess && !on_device) {
+    const size_t bytes = (size_t)members * (size_t)f->P * 4;
+    if (!alloc((void**)&staging, bytes)) {
+      free_field(f);
+      return fail(CORR_E_NOMEM, "device allocation failed for the input staging buffer");
+    }
+    e = cudaMemcpyAsync(staging, values, bytes, cudaMemcpyHostToDevice, st);
+    dvalues = staging;
+  }
+  if (e == cudaSuccess) e = launch_field_ingest(f, dvalues, st);
+  int herr = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, f->err, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (staging) cudaFree(staging);
+  if (e != cudaSuccess) {
+    free_field(f);
+    return cuda_fail(e, "corr_field_create");
+  }
+  if (herr & 2) {
+    free_field(f);
+    return fail(CORR_E_INVAL, "non-finite input value (SPEC.md:72)");
+  }
+  *out = f;
+  return CORR_OK;
+}
+
+int corr_field_destroy(corr_field* f) {
+  if (!f) return CORR_OK;
+  DeviceGuard guard(f->device);
+  cudaDeviceSynchronize();
+  free_field(f);
+  return CORR_OK;
+}
+
+int corr_field_info(const corr_field* f, int32_t* nx, int32_t* ny, int32_t* nz, int32_t* members, int32_t* device) {
+  if (!f) return fail(CORR_E_INVAL, "field is NULL");
+  if (nx) *nx = f->nx;
+  if (ny) *ny = f->ny;
+  if (nz) *nz = f->nz;
+  if (members) *members = f->n;
+  if (device) *device = f->device;
+  return CORR_OK;
+}
+
+static int eval_pairs_impl(const corr_field* fa, const corr_field* fb, int32_t measure, int32_t k,
+                           const int64_t* idxA, const int64_t* idxB, int64_t npairs, float* out, float* dbg_eps,
+                           int32_t* dbg_nx, int32_t* dbg_ny, void* cuda_stream) {
+  int rc = check_pair_fields(fa, fb);
+  if (rc) return rc;
+  rc = resolve_k(fa, measure, k);
+  if (rc) return rc;
+  if (npairs < 0) return fail(CORR_E_INVAL, "npairs < 0");
+  if (npairs == 0) return CORR_OK;
+  if (!idxA || !idxB || !out) return fail(CORR_E_INVAL, "NULL index or output pointer");
+  DeviceGuard guard(fa->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  PairSrc src;
+  memset(&src, 0, sizeof(src));
+  src.mode = kList;
+  src.idxA = idxA;
+  src.idxB = idxB;
+  src.nunits = npairs;
+  src.nx = fa->nx;
+  src.ny = fa->ny;
+  src.P = fa->P;
+  src.same_field = fa == fb;
+  src.err = fa->err;
+  PairOut po;
+  memset(&po, 0, sizeof(po));
+  po.out = out;
+  po.dbg_eps = dbg_eps;
+  po.dbg_nx = dbg_nx;
+  po.dbg_ny = dbg_ny;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  cudaError_t e;
+  if ((measure & 0xFF) == CORR_KSG) {
+    e = launch_ksg(fa, fb, k, (measure & CORR_F_KSG_PLUS1) != 0, src, po, st);
+    if (e == cudaErrorNotSupported) return fail(CORR_E_INVAL, "KSG with k > 8 is not implemented yet");
+  } else {
+    e = launch_pearson_pairs(fa, fb, src, po, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "corr_eval_pairs");
+  return CORR_OK;
+}
+
+int corr_eval_pairs(const corr_field* fa, const corr_field* fb, int32_t measure, int32_t k, const int64_t* idxA,
+                    const int64_t* idxB, int64_t npairs, float* out, void* cuda_stream) {
+  return eval_pairs_impl(fa, fb, measure, k, idxA, idxB, npairs, out, nullptr, nullptr, nullptr, cuda_stream);
+}
+
+int corr_ksg_debug(const corr_field* fa, const corr_field* fb, int32_t k, const int64_t* idxA, const int64_t* idxB,
+                   int64_t npairs, float* eps, int32_t* nx, int32_t* ny, void* cuda_stream) {
+  if (!eps || !nx || !ny) return fail(CORR_E_INVAL, "NULL debug output pointer");
+  if (!fa) return fail(CORR_E_INVAL, "field is NULL");
+  if (npairs <= 0) return npairs == 0 ? CORR_OK : fail(CORR_E_INVAL, "npairs < 0");
+  DeviceGuard guard(fa->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  float* tmp = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&tmp, (size_t)npairs * 4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "corr_ksg_debug");
+  const int rc = eval_pairs_impl(fa, fb, CORR_KSG, k, idxA, idxB, npairs, tmp, eps, nx, ny, cuda_stream);
+  cudaFreeAsync(tmp, st);
+  return rc;
+}
+
+int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure, int32_t k, const corr_box* regionA,
+                    const corr_box* regionB, int64_t nregion_pairs, int64_t samples, uint64_t seed, float* out_max,
+                    int64_t* out_argmax, void* cuda_stream) {
+  const corr_field* fb_in = fb;
+  int rc = check_pair_fields(fa, fb);
+  if (rc) return rc;
+  rc = resolve_k(fa, measure, k);
+  if (rc) return rc;
+  if (nregion_pairs < 0) return fail(CORR_E_INVAL, "nregion_pairs < 0");
+  if (nregion_pairs == 0) return CORR_OK;
+  if (!regionA || !regionB || !out_max || !out_argmax) return fail(CORR_E_INVAL, "NULL region or output pointer");
+  if (samples < 0 || samples >= (int64_t)1 << 32) return fail(CORR_E_INVAL, "samples must be in [0, 2^32)");
+  std::vector<RegionDev> reg((size_t)nregion_pairs);
+  int64_t total = 0;
+  for (int64_t r = 0; r < nregion_pairs; ++r) {
+    const corr_box* bx[2] = {&regionA[r], &regionB[r]};
+    for (int s = 0; s < 2; ++s) {
+      const corr_box& b = *bx[s];
+      if (b.x1 <= b.x0 || b.y1 <= b.y0 || b.z1 <= b.z0) return fail(CORR_E_INVAL, "empty region box");
+      if (b.x0 < 0 || b.y0 < 0 || b.z0 < 0 || b.x1 > fa->nx || b.y1 > fa->ny || b.z1 > fa->nz)
+        return fail(CORR_E_RANGE, "region box outside the grid");
+    }
+    RegionDev& R = reg[(size_t)r];
+    R.A = regionA[r];
+    R.B = regionB[r];
+    R.nA = (int64_t)(R.A.x1 - R.A.x0) * (R.A.y1 - R.A.y0) * (R.A.z1 - R.A.z0);
+    R.nB = (int64_t)(R.B.x1 - R.B.x0) * (R.B.y1 - R.B.y0) * (R.B.z1 - R.B.z0);
+    R.key = region_key(seed, R.A, R.B);
+    R.off = total;
+    if (samples == 0 && R.nA * R.nB >= ((int64_t)1 << 32))
+      return fail(CORR_E_INVAL, "exhaustive region pair with |A|*|B| >= 2^32");
+    total += samples > 0 ? samples : R.nA * R.nB;
+  }
+  DeviceGuard guard(fa->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  RegionDev* dreg = nullptr;
+  unsigned long long* keys = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&dreg, reg.size() * sizeof(RegionDev), st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&keys, (size_t)nregion_pairs * 8, st);
+  if (e != cudaSuccess) return cuda_fail(e, "corr_region_max alloc");
+  e = cudaMemcpyAsync(dreg, reg.data(), reg.size() * sizeof(RegionDev), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(keys, 0, (size_t)nregion_pairs * 8, st);
+
+  PairSrc src;
+  memset(&src, 0, sizeof(src));
+  src.mode = samples > 0 ? kSampled : kExhaustive;
+  src.reg = dreg;
+  src.nreg = nregion_pairs;
+  src.samples = samples;
+  src.nunits = total;
+  src.nx = fa->nx;
+  src.ny = fa->ny;
+  src.P = fa->P;
+  src.same_field = (fb_in == nullptr || fb_in == fa);
+  src.err = fa->err;
+  PairOut po;
+  memset(&po, 0, sizeof(po));
+  po.keys = keys;
+  po.absval = (measure & CORR_F_ABS) != 0;
+  if (e == cudaSuccess) {
+    if ((measure & 0xFF) == CORR_KSG) {
+      e = launch_ksg(fa, fb, k, (measure & CORR_F_KSG_PLUS1) != 0, src, po, st);
+      if (e == cudaErrorNotSupported) {
+        cudaFreeAsync(dreg, st);
+        cudaFreeAsync(keys, st);
+        return fail(CORR_E_INVAL, "KSG with k > 8 is not implemented yet");
+      }
+    } else if (samples == 0) {
+      e = launch_pearson_block(fa, fb, reg.data(), dreg, nregion_pairs, po.absval, keys, st);
+      if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        e = launch_pearson_pairs(fa, fb, src, po, st);
+      }
+    } else {
+      e = launch_pearson_pairs(fa, fb, src, po, st);
+    }
+  }
+  if (e == cudaSuccess) e = launch_region_finalize(src, keys, out_max, out_argmax, st);
+  cudaFreeAsync(dreg, st);
+  cudaFreeAsync(keys, st);
+  if (e != cudaSuccess) return cuda_fail(e, "corr_region_max");
+  return CORR_OK;
+}
+
+int corr_check(const corr_field* f, void* cuda_stream) {
+  if (!f) return fail(CORR_E_INVAL, "field is NULL");
+  DeviceGuard guard(f->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "corr_check");
+  int h = 0;
+  e = cudaMemcpy(&h, f->err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "corr_check");
+  if (h & 1) {
+    const int zero = 0;
+    cudaMemcpy(f->err, &zero, sizeof(int), cudaMemcpyHostToDevice);
+    return fail(CORR_E_RANGE, "point index out of range in an earlier call");
+  }
+  return CORR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// corr_internal.cuh -- internal types of libcorr.so (B200 / sm_100a).
+// The field layout and pair-source abstraction shared by every kernel of the hot
+// path.  Nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "corr.h"
+
+struct corr_field {
+  int device;
+  int nx, ny, nz;
+  int n;          // members
+  int n_pad;      // ceil(n/8)*8: rows are 32-byte aligned, tf32 K multiple of 8
+  int64_t P;      // points
+  float* F;       // [P][n_pad] member-contiguous raw values, pad = 0
+  float* Z;       // [P][n_pad] (x - mean)/||x - mean|| (fp64 -> fp32), pad = 0
+  float* Zhi;     // [P][n_pad] tf32(Z)               (split-TF32 high part)
+  float* Zlo;     // [P][n_pad] tf32(Z - Zhi)         (split-TF32 low part)
+  float* S;       // [P][n_pad] row sorted ascending, pad = +inf
+  uint16_t* perm; // [P][n_pad] argsort of the row (S[p][t] = F[p][perm[p][t]])
+  uint8_t* cflag; // [P] 1 = constant series (min == max)
+  double* psi;    // [n + 2] digamma at integers, psi[0] = NaN
+  int* err;       // device status word: bit0 = index out of range, bit1 = non-finite input
+  void* tmaps;    // lazily built TMA descriptors (pearson_gemm.cu)
+};
+
+namespace corr {
+
+constexpr int kSMs = 148;
+
+// A region pair on the device (boxes, sampler key, sizes, exhaustive offsets).
+struct RegionDev {
+  corr_box A, B;
+  uint64_t key;  // sampler key h_12 (reading R15)
+  int64_t nA, nB;
+  int64_t off;   // exhaustive mode: prefix sum of nA*nB
+};
+
+enum PairMode { kList = 0, kSampled = 1, kExhaustive = 2 };
+
+struct PairSrc {
+  int mode;
+  const int64_t* idxA;
+  const int64_t* idxB;
+  const RegionDev* reg;
+  int64_t nreg;
+  int64_t samples;
+  int64_t nunits;
+  int nx, ny;
+  int64_t P;
+  int same_field;
+  int* err;
+};
+
+struct PairOut {
+  float* out;                // kList: [npairs]
+  unsigned long long* keys;  // kSampled / kExhaustive: [nreg] packed (value, index)
+  int absval;
+  float* dbg_eps;            // optional debug dumps [npairs][n]
+  int32_t* dbg_nx;
+  int32_t* dbg_ny;
+};
+
+// ---- launchers (defined in the .cu files) ----
+cudaError_t launch_field_ingest(corr_field* f, const float* dvalues_member_major, cudaStream_t st);
+cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1,
+                       const PairSrc& src, const PairOut& out, cudaStream_t st);
+cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
+                                 const PairOut& out, cudaStream_t st);
+cudaError_t launch_region_finalize(const PairSrc& src, const unsigned long long* keys,
+                                   float* out_max, int64_t* out_argmax, cudaStream_t st);
+// tcgen05 split-TF32 block GEMM with fused max/argmax epilogue (pearson_gemm.cu).
+// Returns cudaErrorNotSupported if a region shape is not tileable (caller falls back).
+cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, const RegionDev* hreg,
+                                 const RegionDev* dreg, int64_t nreg, int absval,
+                                 unsigned long long* keys, cudaStream_t st);
+
+}  // namespace corr

@@ -1,0 +1,181 @@
+// field.cu -- field ingest, SURVEY.md §8(a) row a1 (§3).
+//
+// Input : float32 [n][P] (member-major file order), device-resident.
+// Output: member-contiguous rows, one 32-byte-aligned row per grid point, so that a
+//         point pair's 2n member values are two contiguous HBM reads (row a2) and a
+//         region block is a dense K-major matrix for the tensor cores (row a7):
+//   F  [P][n_pad]  raw values (pad 0)
+//   Z  [P][n_pad]  standardised series (x - mean)/||x - mean||, fp64 -> fp32
+//                  (Pearson = <Z_a, Z_b>, "means and variances")
+//   Zhi, Zlo       split-TF32 planes: Zhi = tf32_rna(Z), Zlo = tf32_rna(Z - Zhi)
+//   S, perm        row sorted ascending (+inf pad) and its argsort (uint16)
+//   cflag          constant series (min == max) -> NaN correlations (reading R10)
+// All kernels are HBM-bound; DESIGN.md lists their algorithmic bytes.
+#include <math.h>
+
+#include "corr_internal.cuh"
+
+namespace corr {
+namespace {
+
+// ---- 1. transpose [n][P] -> F[P][n_pad] through a 32x32 shared tile -----------
+__global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict__ in, float* __restrict__ F,
+                                                        int n, int n_pad, int64_t P, int* err) {
+  __shared__ float tile[32][33];
+  const int64_t p0 = (int64_t)blockIdx.x * 32;
+  const int m0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < 32; r += 8) {
+    const int m = m0 + ty + r;
+    const int64_t p = p0 + tx;
+    float v = 0.f;
+    if (m < n && p < P) {
+      v = in[(int64_t)m * P + p];
+      bad |= !isfinite(v);
+    }
+    tile[ty + r][tx] = v;
+  }
+  if (bad) atomicOr(err, 2);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 32; r += 8) {
+    const int64_t p = p0 + ty + r;
+    const int m = m0 + tx;
+    if (p < P && m < n_pad) F[p * n_pad + m] = tile[tx][ty + r];
+  }
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- 2. per-point statistics, standardisation, tf32 split (one warp per row) ---
+__global__ void __launch_bounds__(256) stats_kernel(const float* __restrict__ F, float* __restrict__ Z,
+                                                    float* __restrict__ Zhi, float* __restrict__ Zlo,
+                                                    uint8_t* __restrict__ cflag, int n, int n_pad,
+                                                    int64_t P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= P) return;
+  const float* row = F + p * n_pad;
+  double s = 0.0;
+  float mn = INFINITY, mx = -INFINITY;
+  for (int e = lane; e < n; e += 32) {
+    const float v = row[e];
+    s += (double)v;
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+  }
+  s = warp_sum(s);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  const double mean = s / (double)n;
+  double ss = 0.0;
+  for (int e = lane; e < n; e += 32) {
+    const double d = (double)row[e] - mean;
+    ss += d * d;
+  }
+  ss = warp_sum(ss);
+  const bool constant = (mn == mx);
+  const double inv = constant ? 0.0 : 1.0 / sqrt(ss);
+  for (int e = lane; e < n_pad; e += 32) {
+    float z = 0.f;
+    if (e < n && !constant) z = (float)(((double)row[e] - mean) * inv);
+    const float hi = tf32_rna(z);
+    const float lo = tf32_rna(z - hi);
+    Z[p * n_pad + e] = z;
+    Zhi[p * n_pad + e] = hi;
+    Zlo[p * n_pad + e] = lo;
+  }
+  if (lane == 0) cflag[p] = constant ? 1 : 0;
+}
+
+// ---- 3. per-row bitonic sort with argsort (shared memory) ----------------------
+// A group of N2/2 threads sorts one row of N2 = next_pow2(n) (value, index) pairs.
+__global__ void __launch_bounds__(512) sort_kernel(const float* __restrict__ F, float* __restrict__ S,
+                                                   uint16_t* __restrict__ perm, int n, int n_pad,
+                                                   int64_t P, int log2n2) {
+  extern __shared__ unsigned char smem_raw[];
+  const int N2 = 1 << log2n2;
+  const int tpr = min(N2 >> 1, 512);                 // threads per row
+  const int rows_per_block = blockDim.x / tpr;
+  const int g = threadIdx.x / tpr, t = threadIdx.x % tpr;
+  float* sv = reinterpret_cast<float*>(smem_raw) + g * N2;
+  uint16_t* si = reinterpret_cast<uint16_t*>(reinterpret_cast<float*>(smem_raw) + rows_per_block * N2) + g * N2;
+  const int64_t p = (int64_t)blockIdx.x * rows_per_block + g;
+  const bool live = p < P;
+  for (int e = t; e < N2; e += tpr) {
+    sv[e] = (live && e < n) ? F[p * n_pad + e] : INFINITY;
+    si[e] = (uint16_t)(e < n ? e : 0xFFFF);
+  }
+  __syncthreads();
+  for (int size = 2; size <= N2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int c = t; c < (N2 >> 1); c += tpr) {
+        const int lo = 2 * c - (c & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const float a = sv[lo], b = sv[hi];
+        if ((a > b) == asc) {
+          sv[lo] = b; sv[hi] = a;
+          const uint16_t ia = si[lo];
+          si[lo] = si[hi]; si[hi] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (live) {
+    for (int e = t; e < n_pad; e += tpr) {
+      S[p * n_pad + e] = e < n ? sv[e] : INFINITY;
+      perm[p * n_pad + e] = e < n ? si[e] : (uint16_t)0xFFFF;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st) {
+  const int64_t P = f->P;
+  {
+    dim3 grid((unsigned)((P + 31) / 32), (unsigned)((f->n_pad + 31) / 32));
+    transpose_kernel<<<grid, 256, 0, st>>>(din, f->F, f->n, f->n_pad, P, f->err);
+  }
+  {
+    const int64_t threads = P * 32;
+    stats_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(f->F, f->Z, f->Zhi, f->Zlo, f->cflag,
+                                                                   f->n, f->n_pad, P);
+  }
+  {
+    int log2n2 = 1;
+    while ((1 << log2n2) < f->n) ++log2n2;
+    const int N2 = 1 << log2n2;
+    const int tpr = N2 / 2 < 512 ? N2 / 2 : 512;
+    int threads = 512;
+    if (threads < tpr) threads = tpr;
+    const int rows_per_block = threads / tpr;
+    const size_t smem = (size_t)rows_per_block * N2 * (sizeof(float) + sizeof(uint16_t));
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    const int64_t blocks = (P + rows_per_block - 1) / rows_per_block;
+    sort_kernel<<<(unsigned)blocks, threads, smem, st>>>(f->F, f->S, f->perm, f->n, f->n_pad, P, log2n2);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace corr

@@ -1,0 +1,118 @@
+// pearson.cu -- Pearson (PPMCC) for batches of point pairs, SURVEY.md §8(a) row a6,
+// and the region-pair max/argmax finalisation, row a9.
+//
+// PAPER.md:169 (§3.2): "PPMCC requires merely to compute means and variances".  The
+// field stores each series standardised in fp64 (field.cu), so r = <Z_a, Z_b>: one
+// fp32 dot product of two contiguous rows, 8n bytes per pair -- an HBM/L2-bound gather
+// (DESIGN.md).  One warp per pair, float4 loads, fp32 FMA, warp-shuffle reduction,
+// clamp to [-1, 1].
+#include <math.h>
+
+#include "sampler.cuh"
+
+namespace corr {
+namespace {
+
+__global__ void __launch_bounds__(256) pearson_pairs_kernel(const float* __restrict__ Za, const float* __restrict__ Zb,
+                                                            const uint8_t* __restrict__ ca,
+                                                            const uint8_t* __restrict__ cb, int n_pad, PairSrc src,
+                                                            PairOut out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp0; u < src.nunits; u += nwarps) {
+    int64_t a, b, r;
+    uint32_t idx;
+    const bool ok = unit_pair(src, u, a, b, r, idx);
+    if (!ok) {
+      if (src.mode == kList && lane == 0) out.out[u] = NAN;
+      continue;
+    }
+    float acc = 0.f;
+    if (!(ca[a] | cb[b])) {
+      const float4* pa = reinterpret_cast<const float4*>(Za + a * n_pad);
+      const float4* pb = reinterpret_cast<const float4*>(Zb + b * n_pad);
+      const int nq = n_pad >> 2;
+      float acc1 = 0.f;
+      int q = lane;
+      for (; q + 32 < nq; q += 64) {
+        const float4 x0 = __ldg(pa + q), y0 = __ldg(pb + q);
+        const float4 x1 = __ldg(pa + q + 32), y1 = __ldg(pb + q + 32);
+        acc = fmaf(x0.x, y0.x, acc); acc = fmaf(x0.y, y0.y, acc);
+        acc = fmaf(x0.z, y0.z, acc); acc = fmaf(x0.w, y0.w, acc);
+        acc1 = fmaf(x1.x, y1.x, acc1); acc1 = fmaf(x1.y, y1.y, acc1);
+        acc1 = fmaf(x1.z, y1.z, acc1); acc1 = fmaf(x1.w, y1.w, acc1);
+      }
+      if (q < nq) {
+        const float4 x0 = __ldg(pa + q), y0 = __ldg(pb + q);
+        acc = fmaf(x0.x, y0.x, acc); acc = fmaf(x0.y, y0.y, acc);
+        acc = fmaf(x0.z, y0.z, acc); acc = fmaf(x0.w, y0.w, acc);
+      }
+      acc += acc1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      acc = fminf(1.f, fmaxf(-1.f, acc));
+    } else {
+      acc = NAN;
+    }
+    if (lane == 0) {
+      if (src.mode == kList) {
+        out.out[u] = acc;
+      } else if (!isnan(acc)) {
+        atomicMax(out.keys + r, pack_key(out.absval ? fabsf(acc) : acc, idx));
+      }
+    }
+  }
+}
+
+__global__ void region_finalize_kernel(PairSrc src, const unsigned long long* __restrict__ keys,
+                                       float* __restrict__ out_max, int64_t* __restrict__ out_arg) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= src.nreg) return;
+  const unsigned long long key = keys[r];
+  if (key == 0ULL) {
+    out_max[r] = NAN;
+    out_arg[2 * r] = -1;
+    out_arg[2 * r + 1] = -1;
+    return;
+  }
+  const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFULL);
+  const RegionDev& R = src.reg[r];
+  int64_t a, b;
+  if (src.mode == kSampled) {
+    const uint64_t v = mix64(R.key + kGolden * (uint64_t)((int64_t)idx + 1));
+    a = box_to_point(R.A, (int64_t)(((v & 0xFFFFFFFFULL) * (uint64_t)R.nA) >> 32), src.nx, src.ny);
+    b = box_to_point(R.B, (int64_t)(((v >> 32) * (uint64_t)R.nB) >> 32), src.nx, src.ny);
+  } else {
+    const int64_t q = (int64_t)idx;
+    a = box_to_point(R.A, q / R.nB, src.nx, src.ny);
+    b = box_to_point(R.B, q % R.nB, src.nx, src.ny);
+  }
+  out_max[r] = unpack_value(key);
+  out_arg[2 * r] = a;
+  out_arg[2 * r + 1] = b;
+}
+
+}  // namespace
+
+cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
+                                 const PairOut& out, cudaStream_t st) {
+  if (src.nunits == 0) return cudaSuccess;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pearson_pairs_kernel, 256, 0);
+  if (occ < 1) occ = 1;
+  int64_t blocks = (src.nunits + 7) / 8;
+  const int64_t cap = (int64_t)kSMs * occ * 4;
+  if (blocks > cap) blocks = cap;
+  pearson_pairs_kernel<<<(unsigned)blocks, 256, 0, st>>>(fa->Z, fb->Z, fa->cflag, fb->cflag, fa->n_pad, src, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_region_finalize(const PairSrc& src, const unsigned long long* keys, float* out_max,
+                                   int64_t* out_argmax, cudaStream_t st) {
+  if (src.nreg == 0) return cudaSuccess;
+  region_finalize_kernel<<<(unsigned)((src.nreg + 127) / 128), 128, 0, st>>>(src, keys, out_max, out_argmax);
+  return cudaGetLastError();
+}
+
+}  // namespace corr
