@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the arXiv 2309.03308 hot path on 1..8 B200s.
+
+Workload (BASELINE.json metric "KSG-MI pairs/s (1000 members)", configs[3]): the
+context view of a 250x352x20 synthetic ensemble with n = 1000 members, 88 bricks of
+32x32x20 -> 3828 region pairs, S random point pairs per region pair (default 4096),
+KSG MI k = 3 reduced to per-region-pair max/argmax.  One STEP = one pass of the whole
+hot path over the context view:
+    KSG region max (rows a2-a5, a8, a9)  +  Pearson sampled region max (a6)
+    +  Pearson exhaustive focus block on the two cluster bricks (a7, tcgen05 GEMM)
+    +  all-gather of the shards' maxima over NCCL (a10, N > 1).
+`value` = KSG point pairs evaluated per second by the whole job (max-over-ranks device
+time), inputs resident in HBM.  `e2e` = the same metric through the C ABI starting from
+HOST memory: per step the 7 GB member-major field is copied from pinned host memory,
+ingested (corr_field_create), the step runs, and the maxima are read back to the host.
+
+`--impl reference` times the CPU oracle (oracle/, plain C + OpenMP) as it stands on the
+box's host cores on a bounded sample of the same workload (the reference arm for this
+paper-only tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as tdist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2309_03308_b200 import binding as cb  # noqa: E402
+from paper_2309_03308_b200 import dist as cdist  # noqa: E402
+from paper_2309_03308_b200 import synth  # noqa: E402
+
+METRIC = "KSG-MI pairs/s (1000 members)"
+UNIT = "pairs/s"
+K_NN = 3
+SEED = 20230907
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                power.append(float(parts[7]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# --------------------------------------------------------------------------- workload
+def workload(samples: int):
+    cfg = synth.C4
+    spec = synth.spec_of(cfg)
+    A, B = synth.context_pairs(synth.bricks_of(cfg))
+    return cfg, spec, A, B
+
+
+def focus_boxes():
+    # the two bricks holding the large cluster centres
+    return synth.C2_REGION_A, synth.C2_REGION_B
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample_run(spec, A, B, samples, npairs, seed):
+    """Times the oracle (as it stands) on the first `npairs` sampled pairs of the workload."""
+    import oracle
+    pairs = []
+    r = 0
+    while len(pairs) < npairs:
+        for s in range(min(samples, npairs - len(pairs))):
+            pairs.append(oracle.sample(seed, A[r], B[r], s, spec.nx, spec.ny))
+        r += 1
+    pts = sorted({p for ab in pairs for p in ab})
+    pos = {p: i for i, p in enumerate(pts)}
+    mini = synth.rows(spec, torch.tensor(pts)).T.contiguous().numpy()
+    ia = np.array([pos[a] for a, _ in pairs], np.int64)
+    ib = np.array([pos[b] for _, b in pairs], np.int64)
+    oracle.lib()
+    t = time.perf_counter()
+    vals = oracle.eval_pairs(mini, None, oracle.KSG, K_NN, ia, ib)
+    dt = time.perf_counter() - t
+    return npairs / dt, dt, vals
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg, spec, A, B = workload(args.samples)
+    cores = cpu_count()
+    npairs = args.ref_pairs
+    times = []
+    for i in range(args.warmup + args.steps):
+        _, dt, _ = oracle_sample_run(spec, A, B, args.samples, npairs, SEED + i)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * float(np.mean(times))
+    value = npairs / (ms / 1e3)
+    sample = (f"{npairs} sampled point pairs of the C4 context view per step (n=1000, k=3), "
+              f"oracle.eval_pairs brute force, OpenMP over pairs")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(cfg, args, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, args, world):
+    return {"workload": f"C4 context view: 250x352x20 grid, n=1000 members, 88 bricks 32x32x20, 3828 region "
+                        f"pairs x S={args.samples} sampled point pairs, KSG k=3 region max (+ Pearson sampled "
+                        f"region max + Pearson exhaustive focus block)",
+            "grid": [cfg.nx, cfg.ny, cfg.nz], "members": cfg.members, "k": K_NN, "region_pairs": 3828,
+            "samples_per_region_pair": args.samples, "parallelism": f"region-pair shards x{world}",
+            "l2": "inputs larger than L2 (field rows 7 GB x planes, random rows per pair)"}
+
+
+# --------------------------------------------------------------------------- our arm
+def make_field(spec, device, values=None):
+    vals = synth.generate(spec, device=f"cuda:{device}") if values is None else values
+    f = cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members, device=device)
+    return f, vals
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--samples", type=int, default=4096)
+    ap.add_argument("--ref-pairs", type=int, default=192)
+    ap.add_argument("--cpu-pairs", type=int, default=768)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, spec, A, B = workload(args.samples)
+    R = len(A)
+    S = args.samples
+    bounds = cdist.shard_bounds([S] * R, world)
+    lo, hi = bounds[rank]
+    Ash, Bsh = cb.boxes(A[lo:hi]), cb.boxes(B[lo:hi])
+    fA, fB = focus_boxes()
+    slabs = cdist.split_box_z(fA, world)
+    myslab = cb.boxes([slabs[rank]])
+    fBb = cb.boxes([fB])
+
+    # field replica: rank 0 generates, NCCL broadcast to the others (untimed here)
+    vals = torch.empty((spec.members, spec.points), dtype=torch.float32, device=f"cuda:{local}")
+    if rank == 0:
+        vals.copy_(synth.generate(spec, device=f"cuda:{local}"))
+    if world > 1:
+        tdist.broadcast(vals, 0)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    field = cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members, device=local)
+    create_s = time.perf_counter() - t
+
+    stream = torch.cuda.current_stream()
+    kev = []
+
+    def step(f, timed=False):
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        km, ka = cb.corr_region_max(f, None, cb.CORR_KSG, K_NN, Ash, Bsh, S, SEED)
+        if timed:
+            e1.record(stream)
+            kev.append((e0, e1))
+        pm, pa = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, Ash, Bsh, S, SEED)
+        fm, fa = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, myslab, fBb, 0, 0)
+        if world > 1:
+            km, ka = cdist.gather_region_results(km, ka, bounds)
+            pm, pa = cdist.gather_region_results(pm, pa, bounds)
+            fparts = [torch.empty((1, 3), dtype=torch.int64, device=fm.device) for _ in range(world)]
+            packed = torch.cat([fm.view(torch.int32).to(torch.int64).view(1, 1), fa.view(1, 2)], 1)
+            tdist.all_gather(fparts, packed)
+            fm = torch.stack([p[0, 0].to(torch.int32).view(torch.float32) for p in fparts])
+            fa = torch.stack([p[0, 1:] for p in fparts])
+        return km, ka, pm, pa, fm, fa
+
+    for _ in range(args.warmup):
+        step(field)
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    l0 = cb.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        res = step(field, timed=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = cb.launch_count() - l0
+    if world > 1:
+        tdist.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    ksg_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    if world > 1:
+        tt = torch.tensor([ms, ksg_ms], dtype=torch.float64, device=f"cuda:{local}")
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        ms, ksg_ms = float(tt[0]), float(tt[1])
+    total_pairs = R * S
+    value = total_pairs / (ms / 1e3)
+
+    # roofline of the dominant kernel (KSG k-NN, ALU-bound): algorithmic member-comparisons
+    n = spec.members
+    my_pairs = (hi - lo) * S
+    achieved = my_pairs * n * (n - 1) / (ksg_ms / 1e3)
+    peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
+    sm_max = peaks.get("sm_max_mhz") or clk.get("sm_max_mhz") or 1965.0
+    peak = 148 * 128 * sm_max * 1e6 / 4.0
+    traffic = None
+    if os.path.exists(NCU_TRAFFIC):
+        try:
+            tr = json.load(open(NCU_TRAFFIC))
+            traffic = tr.get("ksg_bytes_per_pair", 0) * my_pairs or None
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "ksg_kernel<3,8> (k-NN + counts + psi)", "achieved": achieved / 1e9,
+                "peak": peak / 1e9, "unit": "Gcmp/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_basis": f"148 SMs x 128 fp32 lanes x {sm_max:.0f} MHz / 4 ops per comparison",
+                "frac_at_measured_clock": (achieved / (148 * 128 * clk["sm_mhz"] * 1e6 / 4.0)
+                                           if clk.get("sm_mhz") else None),
+                "ksg_ms_per_step": ksg_ms}
+
+    # e2e: same metric from HOST memory through the C ABI (field upload + ingest per step)
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((spec.members, spec.points), dtype=torch.float32, pin_memory=True) if rank == 0 else None
+        if rank == 0:
+            host.copy_(vals)
+        del field
+        torch.cuda.empty_cache()
+        h2d = spec.members * spec.points * 4 + 2 * (hi - lo) * 80 + 80
+        d2h = 0
+
+        def e2e_step():
+            nonlocal d2h
+            if rank == 0:
+                vals.copy_(host, non_blocking=True)
+            if world > 1:
+                tdist.broadcast(vals, 0)
+            f = cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members, device=local)
+            out = step(f)
+            outs = [o.to("cpu") for o in out]
+            d2h = sum(o.numel() * o.element_size() for o in outs)
+            f.close()
+            return outs
+
+        e2e_step()
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        te = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 2))):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_s = (time.perf_counter() - te) / max(1, min(args.steps, 2))
+        if world > 1:
+            tt = torch.tensor([e_s], dtype=torch.float64, device=f"cuda:{local}")
+            tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+            e_s = float(tt[0])
+        e2e = {"value": total_pairs / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d if rank == 0 else 0,
+               "d2h_bytes_per_step": d2h, "s_per_step": e_s,
+               "includes": "pinned-host field upload (7.04 GB) + NCCL broadcast + corr_field_create + step + D2H"}
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, _ = oracle_sample_run(spec, A, B, S, args.cpu_pairs, SEED)
+        cpu_base = {"value": v, "unit": UNIT, "cores": cpu_count(), "kind": "oracle",
+                    "sample": f"first {args.cpu_pairs} sampled pairs of the C4 context view (n=1000, k=3), "
+                              f"oracle.eval_pairs, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, args, world),
+                "roofline": roofline, "cpu_baseline": cpu_base, "e2e": e2e, "clocks": clk,
+                "gpu_launches": launches, "field_create_s": create_s,
+                "region_max_sample": [float(res[0][0]), int(res[1][0][0]), int(res[1][0][1])]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -125,6 +125,10 @@ int corr_ksg_debug(const corr_field* fa, const corr_field* fb, int32_t k, const 
  * CUDA error, else CORR_OK. */
 int corr_check(const corr_field* f, void* cuda_stream);
 
+/* Number of CUDA kernels this library has launched in this process (diagnostic; bench.py
+ * reports the launches inside its timed region as `gpu_launches`). */
+int64_t corr_launch_count(void);
+
 /* Thread-local message for the last non-OK status of this thread ("" if none). */
 const char* corr_last_error(void);
 

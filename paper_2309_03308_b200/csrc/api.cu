@@ -13,6 +13,8 @@
 
 using namespace corr;
 
+std::atomic<long long> corr::g_launch_count{0};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -106,6 +108,8 @@ int resolve_k(const corr_field* f, int32_t measure, int32_t& k) {
 extern "C" {
 
 const char* corr_last_error(void) { return g_last_error.c_str(); }
+
+int64_t corr_launch_count(void) { return (int64_t)g_launch_count.load(); }
 
 int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t device,
                       void* cuda_stream, corr_field** out) {

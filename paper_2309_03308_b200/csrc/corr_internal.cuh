@@ -26,9 +26,13 @@ struct corr_field {
   void* tmaps;    // lazily built TMA descriptors (pearson_gemm.cu)
 };
 
+#include <atomic>
+
 namespace corr {
 
 constexpr int kSMs = 148;
+extern std::atomic<long long> g_launch_count;  // kernels launched (corr_launch_count)
+inline void note_launch(int k = 1) { g_launch_count.fetch_add(k, std::memory_order_relaxed); }
 
 // A region pair on the device (boxes, sampler key, sizes, exhaustive offsets).
 struct RegionDev {

@@ -175,6 +175,7 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
     const int64_t blocks = (P + rows_per_block - 1) / rows_per_block;
     sort_kernel<<<(unsigned)blocks, threads, smem, st>>>(f->F, f->S, f->perm, f->n, f->n_pad, P, log2n2);
   }
+  note_launch(3);
   return cudaGetLastError();
 }
 

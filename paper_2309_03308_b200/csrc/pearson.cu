@@ -105,6 +105,7 @@ cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, con
   const int64_t cap = (int64_t)kSMs * occ * 4;
   if (blocks > cap) blocks = cap;
   pearson_pairs_kernel<<<(unsigned)blocks, 256, 0, st>>>(fa->Z, fb->Z, fa->cflag, fb->cflag, fa->n_pad, src, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -112,6 +113,7 @@ cudaError_t launch_region_finalize(const PairSrc& src, const unsigned long long*
                                    int64_t* out_argmax, cudaStream_t st) {
   if (src.nreg == 0) return cudaSuccess;
   region_finalize_kernel<<<(unsigned)((src.nreg + 127) / 128), 128, 0, st>>>(src, keys, out_max, out_argmax);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -15,7 +15,7 @@ from paper_2309_03308_b200 import binding, build
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "corr.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(corr_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(corr_\w+)\s*\(", src, re.M)))
 
 
 def test_library_builds_and_exports_every_declared_symbol():
