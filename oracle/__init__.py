@@ -170,6 +170,53 @@ def sample(seed: int, A, B, s: int, nx: int, ny: int) -> Tuple[int, int]:
     return pa.value, pb.value
 
 
+def _box_points(box, nx, ny):
+    x0, y0, z0, x1, y1, z1 = box
+    z, y, x = np.meshgrid(np.arange(z0, z1), np.arange(y0, y1), np.arange(x0, x1), indexing="ij")
+    return ((z * ny + y) * nx + x).reshape(-1).astype(np.int64)  # local index, x fastest
+
+
+def pearson_block_max(fa, fb, dims, A, B, absval: bool = False, chunk: int = 2048):
+    """Exhaustive Pearson maximum of one region pair -- the PPMCC definition
+    (two-pass fp64 means and deviations) for EVERY pair of the two bricks, with
+    the |A| x |B| sums of products formed by a library fp64 matmul (a permitted primitive).
+    Values rounded to fp32 as the library returns them; NaN (constant series) skipped; ties ->
+    lowest q = a_local*|B| + b_local (R16); self pairs skipped with one field.
+    Returns (max, (a, b)) with (nan, (-1, -1)) if no pair is defined."""
+    nx, ny, nz = dims
+    fa = _field(fa)
+    fbn = fa if fb is None else _field(fb)
+    pa, pb = _box_points(A, nx, ny), _box_points(B, nx, ny)
+
+    def standardise(v):
+        v = v.astype(np.float64)
+        d = v - v.mean(axis=0, keepdims=True)
+        nrm = np.sqrt((d * d).sum(axis=0))
+        with np.errstate(invalid="ignore", divide="ignore"):
+            z = d / nrm
+        return z, nrm == 0.0
+
+    zb, cb = standardise(fbn[:, pb])
+    best, arg = np.nan, (-1, -1)
+    for s in range(0, pa.size, chunk):
+        za, ca = standardise(fa[:, pa[s:s + chunk]])
+        c = za.T @ zb  # [chunk, |B|] sums of products of deviations / norms
+        c = np.clip(c, -1.0, 1.0)
+        if absval:
+            c = np.abs(c)
+        c[ca, :] = np.nan
+        c[:, cb] = np.nan
+        if fb is None:
+            c[pa[s:s + chunk][:, None] == pb[None, :]] = np.nan
+        c = c.astype(np.float32).astype(np.float64)
+        c = np.where(np.isnan(c), -np.inf, c)
+        q = int(np.argmax(c))  # first maximum in row-major (a_local, b_local) order = lowest q
+        v = c.reshape(-1)[q]
+        if np.isfinite(v) and (np.isnan(best) or v > best):
+            best, arg = v, (int(pa[s + q // pb.size]), int(pb[q % pb.size]))
+    return best, arg
+
+
 def region_max(fa, fb, dims, measure: int, k: int, regA, regB, samples: int, seed: int):
     """Returns (out_max float64 [R], out_argmax int64 [R, 2])."""
     nx, ny, nz = dims

@@ -1,8 +1,464 @@
-// pearson_gemm.cu -- placeholder until the tcgen05 block GEMM lands.
-#include "corr_internal.cuh"
+// pearson_gemm.cu -- exhaustive Pearson region-pair maximum as a tcgen05 GEMM,
+// SURVEY.md §8(a) row a7 (+ a9).
+//
+// PAPER.md:133 (§3): the region-pair indicator is the maximum point-pair correlation of
+// two bricks; PAPER.md:45 and :498 note that all point pairs take ">2 days" / "365 days"
+// on the paper's GPU.  With the series standardised in fp64 (field.cu), every Pearson
+// value of a brick pair is one entry of C = Z_A . Z_B^T (|A| x |B|, K = n), a dense
+// contraction that belongs on the 5th-gen tensor cores.  fp32 tolerance (1e-5) is kept
+// with split-TF32: Z = Z_hi + Z_lo (both tf32) and
+//     C ~= Z_hi Z_hi^T + Z_hi Z_lo^T + Z_lo Z_hi^T          (3 tcgen05.mma per k-step)
+// (the dropped Z_lo Z_lo^T term is ~2^-22 relative).  C is never written to memory: the
+// epilogue reduces each 128x256 accumulator tile straight out of TMEM to one packed
+// (value, lowest q) key per thread and a u64 atomicMax per warp (reading R16).
+//
+// Kernel shape (one CTA per SM, persistent over the tiles of all region pairs):
+//   warp 0      TMA producer: 4 tensor-map loads per k-block (A_hi, A_lo, B_hi, B_lo),
+//               K-major, 128-byte swizzle, boxes of 32 members x (points of a brick slab)
+//   warp 1      TMEM owner + single-thread MMA issuer, kind::tf32, M=128 N=256 K=8
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> column mask (region / constant /
+//               self pair) -> per-32-column FMNMX max -> first index of the max ->
+//               (value, q) key -> warp max -> atomicMax
+//   TMEM: 2 accumulators x 256 columns (double-buffered so the epilogue of tile t
+//   overlaps the MMAs of tile t+1); smem: 2 stages x 96 KB.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "sampler.cuh"
+
 namespace corr {
-cudaError_t launch_pearson_block(const corr_field*, const corr_field*, const RegionDev*, const RegionDev*, int64_t,
-                                 int, unsigned long long*, cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
+constexpr int A_BYTES = BM * BK * 4;  // 16 KB per plane
+constexpr int B_BYTES = BN * BK * 4;  // 32 KB per plane
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr int kThreads = 192;
+constexpr uint32_t kTmemCols = 512;
+
+struct GemmRegion {
+  corr_box A, B;
+  int ntA[3], ntB[3];  // tiles along x, y, z
+  int64_t tile_off;    // prefix of mt*nt
+  int64_t nA, nB;
+  int overlap;         // one field and the boxes intersect -> self-pair mask needed
+  int pad;
+};
+
+struct GemmGeom {
+  int bxA, byA, bzA, bxB, byB, bzB;
+  int nx, ny;
+  int kblocks;
+  int absval;
+  int same_field;
+  int64_t nreg;
+  int64_t total_tiles;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// K-major operand, 128-byte swizzle atoms of 8 rows x 128 B (SBO = 1024 B), sm_100 version 1
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// instruction descriptor: D=f32, A=B=tf32, K-major both, N=256, M=128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TileCoord {
+  int64_t r;
+  int tx, ty, tz, ux, uy, uz;  // A tile (tx,ty,tz), B tile (ux,uy,uz)
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const GemmRegion* __restrict__ reg, int64_t nreg, int64_t t) {
+  int64_t lo = 0, hi = nreg - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (reg[mid].tile_off <= t) lo = mid; else hi = mid - 1;
+  }
+  const GemmRegion& R = reg[lo];
+  int64_t q = t - R.tile_off;
+  const int64_t ntB = (int64_t)R.ntB[0] * R.ntB[1] * R.ntB[2];
+  const int64_t mi = q / ntB, ni = q - mi * ntB;
+  TileCoord c;
+  c.r = lo;
+  c.tx = (int)(mi % R.ntA[0]);
+  c.ty = (int)((mi / R.ntA[0]) % R.ntA[1]);
+  c.tz = (int)(mi / ((int64_t)R.ntA[0] * R.ntA[1]));
+  c.ux = (int)(ni % R.ntB[0]);
+  c.uy = (int)((ni / R.ntB[0]) % R.ntB[1]);
+  c.uz = (int)(ni / ((int64_t)R.ntB[0] * R.ntB[1]));
+  return c;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    pearson_block_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                         const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                         const GemmRegion* __restrict__ reg, GemmGeom g, const uint8_t* __restrict__ ca,
+                         const uint8_t* __restrict__ cb, unsigned long long* __restrict__ keys) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-align the operand stages (128-byte swizzle atoms)
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* stage_base = base;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* colbias = reinterpret_cast<float*>(tmem_slot + 4);  // [2][BN]
+  int* colpt = reinterpret_cast<int*>(colbias + 2 * BN);      // [2][BN]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mAhi) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mAlo) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mBhi) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mBlo) : "memory");
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+        const TileCoord c = tile_coord(reg, g.nreg, t);
+        const GemmRegion& R = reg[c.r];
+        const int ax = R.A.x0 + c.tx * g.bxA, ay = R.A.y0 + c.ty * g.byA, az = R.A.z0 + c.tz * g.bzA;
+        const int bx = R.B.x0 + c.ux * g.bxB, by = R.B.y0 + c.uy * g.byB, bz = R.B.z0 + c.uz * g.bzB;
+        for (int kb = 0; kb < g.kblocks; ++kb, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          unsigned char* st = stage_base + s * STAGE_BYTES;
+          mbar_expect_tx(full + s, STAGE_BYTES);
+          tma_load_4d(st, &mAhi, full + s, kb * BK, ax, ay, az);
+          tma_load_4d(st + A_BYTES, &mAlo, full + s, kb * BK, ax, ay, az);
+          tma_load_4d(st + 2 * A_BYTES, &mBhi, full + s, kb * BK, bx, by, bz);
+          tma_load_4d(st + 2 * A_BYTES + B_BYTES, &mBlo, full + s, kb * BK, bx, by, bz);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    uint32_t it = 0, tt = 0;
+    for (int64_t t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++tt) {
+      const uint32_t acc = tt & 1, aph = (tt >> 1) & 1;
+      mbar_wait(tempty + acc, aph ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tmem_base + acc * BN;
+      for (int kb = 0; kb < g.kblocks; ++kb, ++it) {
+        const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+        mbar_wait(full + s, ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = smem_u32(stage_base + s * STAGE_BYTES);
+          const uint64_t dAhi = sdesc_sw128(st), dAlo = sdesc_sw128(st + A_BYTES);
+          const uint64_t dBhi = sdesc_sw128(st + 2 * A_BYTES), dBlo = sdesc_sw128(st + 2 * A_BYTES + B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 bytes inside the swizzle atom
+            const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
+            tc_mma_tf32(dcol, dAhi + adv, dBhi + adv, kIdesc, first);
+            tc_mma_tf32(dcol, dAhi + adv, dBlo + adv, kIdesc, 1u);
+            tc_mma_tf32(dcol, dAlo + adv, dBhi + adv, kIdesc, 1u);
+          }
+          tc_commit(empty + s);  // smem stage free once these MMAs have read it
+        }
+        __syncwarp();
+      }
+      if (lane == 0) tc_commit(tfull + acc);  // accumulator complete
+      __syncwarp();
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int q4 = warp & 3;               // TMEM lane quarter this warp may access
+    const int row = q4 * 32 + lane;        // accumulator row = A point of the tile
+    const int et = threadIdx.x - 64;       // 0..127
+    uint32_t tt = 0;
+    for (int64_t t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++tt) {
+      const uint32_t acc = tt & 1, aph = (tt >> 1) & 1;
+      const TileCoord c = tile_coord(reg, g.nreg, t);
+      const GemmRegion& R = reg[c.r];
+      // per-tile column table (B points): bias 0 / -inf and point id (self-pair mask)
+      float* cbias = colbias + acc * BN;
+      int* cpt = colpt + acc * BN;
+      for (int n = et; n < BN; n += 128) {
+        const int lx = n % g.bxB, ly = (n / g.bxB) % g.byB, lz = n / (g.bxB * g.byB);
+        const int x = R.B.x0 + c.ux * g.bxB + lx, y = R.B.y0 + c.uy * g.byB + ly, z = R.B.z0 + c.uz * g.bzB + lz;
+        bool ok = x < R.B.x1 && y < R.B.y1 && z < R.B.z1;
+        int p = -1;
+        if (ok) {
+          p = (z * g.ny + y) * g.nx + x;
+          ok = cb[p] == 0;
+        }
+        cbias[n] = ok ? 0.f : -INFINITY;
+        cpt[n] = p;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // this thread's row (A point)
+      const int lxA = row % g.bxA, lyA = (row / g.bxA) % g.byA, lzA = row / (g.bxA * g.byA);
+      const int xa = R.A.x0 + c.tx * g.bxA + lxA, ya = R.A.y0 + c.ty * g.byA + lyA, za = R.A.z0 + c.tz * g.bzA + lzA;
+      bool row_ok = xa < R.A.x1 && ya < R.A.y1 && za < R.A.z1;
+      int pa = -1;
+      if (row_ok) {
+        pa = (za * g.ny + ya) * g.nx + xa;
+        row_ok = ca[pa] == 0;
+      }
+      const bool selfmask = R.overlap != 0;
+      mbar_wait(tfull + acc, aph);
+      tc_fence_after();
+      float best = -INFINITY;
+      int bidx = 0;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q4 * 32) << 16);
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        float v[32];
+        tmem_ld32(taddr + ch * 32, v);
+        const float4* b4 = reinterpret_cast<const float4*>(cbias + ch * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 bb = b4[i];
+          v[4 * i + 0] = (g.absval ? fabsf(v[4 * i + 0]) : v[4 * i + 0]) + bb.x;
+          v[4 * i + 1] = (g.absval ? fabsf(v[4 * i + 1]) : v[4 * i + 1]) + bb.y;
+          v[4 * i + 2] = (g.absval ? fabsf(v[4 * i + 2]) : v[4 * i + 2]) + bb.z;
+          v[4 * i + 3] = (g.absval ? fabsf(v[4 * i + 3]) : v[4 * i + 3]) + bb.w;
+        }
+        if (selfmask) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (cpt[ch * 32 + i] == pa) v[i] = -INFINITY;
+        }
+        float m = v[0];
+#pragma unroll
+        for (int i = 1; i < 32; ++i) m = fmaxf(m, v[i]);
+        if (m > best) {
+          int j = 31;
+#pragma unroll
+          for (int i = 31; i >= 0; --i)
+            if (v[i] == m) j = i;
+          best = m;
+          bidx = ch * 32 + j;
+        }
+      }
+      // release the accumulator to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      unsigned long long key = 0ULL;
+      if (row_ok && best > -INFINITY) {
+        best = fminf(1.f, fmaxf(-1.f, best));
+        const int pb = cpt[bidx];
+        const int xb = pb % g.nx, yb = (pb / g.nx) % g.ny, zb = pb / (g.nx * g.ny);
+        const int64_t axs = R.A.x1 - R.A.x0, ays = R.A.y1 - R.A.y0;
+        const int64_t bxs = R.B.x1 - R.B.x0, bys = R.B.y1 - R.B.y0;
+        const int64_t al = ((int64_t)(za - R.A.z0) * ays + (ya - R.A.y0)) * axs + (xa - R.A.x0);
+        const int64_t bl = ((int64_t)(zb - R.B.z0) * bys + (yb - R.B.y0)) * bxs + (xb - R.B.x0);
+        key = pack_key(best, (uint32_t)(al * R.nB + bl));
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+        key = other > key ? other : key;
+      }
+      if (lane == 0 && key != 0ULL) atomicMax(keys + c.r, key);
+      // the column table of this accumulator is rewritten two tiles later; all 4 warps
+      // must be past it before then
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* plane, const corr_field* f, int bx, int by, int bz) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)f->n_pad, (cuuint64_t)f->nx, (cuuint64_t)f->ny, (cuuint64_t)f->nz};
+  cuuint64_t strides[3] = {(cuuint64_t)f->n_pad * 4, (cuuint64_t)f->n_pad * 4 * f->nx,
+                           (cuuint64_t)f->n_pad * 4 * f->nx * f->ny};
+  cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)plane, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int pow2ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// Brick-slab box of `rows` points: x extent first (coalesced), then y, then z.
+void box_shape(int rows, int ax, int ay, int& bx, int& by, int& bz) {
+  bx = pow2ceil(ax) < 32 ? pow2ceil(ax) : 32;
+  by = pow2ceil(ay) < rows / bx ? pow2ceil(ay) : rows / bx;
+  bz = rows / (bx * by);
+}
+
+}  // namespace
+
+cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, const RegionDev* hreg,
+                                 const RegionDev* /*dreg*/, int64_t nreg, int absval, unsigned long long* keys,
+                                 cudaStream_t st) {
+  if (nreg == 0) return cudaSuccess;
+  int maxax = 1, maxay = 1, maxbx = 1, maxby = 1;
+  for (int64_t r = 0; r < nreg; ++r) {
+    const RegionDev& R = hreg[r];
+    maxax = std::max(maxax, R.A.x1 - R.A.x0);
+    maxay = std::max(maxay, R.A.y1 - R.A.y0);
+    maxbx = std::max(maxbx, R.B.x1 - R.B.x0);
+    maxby = std::max(maxby, R.B.y1 - R.B.y0);
+  }
+  GemmGeom g;
+  memset(&g, 0, sizeof(g));
+  box_shape(BM, maxax, maxay, g.bxA, g.byA, g.bzA);
+  box_shape(BN, maxbx, maxby, g.bxB, g.byB, g.bzB);
+  if (g.bzA > 256 || g.bzB > 256) return cudaErrorNotSupported;
+  g.nx = fa->nx;
+  g.ny = fa->ny;
+  g.kblocks = (fa->n_pad + BK - 1) / BK;
+  g.absval = absval;
+  g.same_field = fa == fb;
+  g.nreg = nreg;
+  std::vector<GemmRegion> gr((size_t)nreg);
+  int64_t tiles = 0;
+  for (int64_t r = 0; r < nreg; ++r) {
+    const RegionDev& R = hreg[r];
+    GemmRegion& G = gr[(size_t)r];
+    G.A = R.A;
+    G.B = R.B;
+    G.ntA[0] = (R.A.x1 - R.A.x0 + g.bxA - 1) / g.bxA;
+    G.ntA[1] = (R.A.y1 - R.A.y0 + g.byA - 1) / g.byA;
+    G.ntA[2] = (R.A.z1 - R.A.z0 + g.bzA - 1) / g.bzA;
+    G.ntB[0] = (R.B.x1 - R.B.x0 + g.bxB - 1) / g.bxB;
+    G.ntB[1] = (R.B.y1 - R.B.y0 + g.byB - 1) / g.byB;
+    G.ntB[2] = (R.B.z1 - R.B.z0 + g.bzB - 1) / g.bzB;
+    G.tile_off = tiles;
+    G.nA = R.nA;
+    G.nB = R.nB;
+    G.overlap = g.same_field && R.A.x0 < R.B.x1 && R.B.x0 < R.A.x1 && R.A.y0 < R.B.y1 && R.B.y0 < R.A.y1 &&
+                R.A.z0 < R.B.z1 && R.B.z0 < R.A.z1;
+    tiles += (int64_t)G.ntA[0] * G.ntA[1] * G.ntA[2] * G.ntB[0] * G.ntB[1] * G.ntB[2];
+  }
+  g.total_tiles = tiles;
+  CUtensorMap mAhi, mAlo, mBhi, mBlo;
+  if (!make_map(&mAhi, fa->Zhi, fa, g.bxA, g.byA, g.bzA) || !make_map(&mAlo, fa->Zlo, fa, g.bxA, g.byA, g.bzA) ||
+      !make_map(&mBhi, fb->Zhi, fb, g.bxB, g.byB, g.bzB) || !make_map(&mBlo, fb->Zlo, fb, g.bxB, g.byB, g.bzB))
+    return cudaErrorNotSupported;
+  GemmRegion* dgr = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&dgr, gr.size() * sizeof(GemmRegion), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(dgr, gr.data(), gr.size() * sizeof(GemmRegion), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16 + 2 * BN * 4 + 2 * BN * 4;
+  e = cudaFuncSetAttribute(pearson_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = kSMs;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = tiles < sms ? tiles : sms;
+  pearson_block_kernel<<<(unsigned)grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag,
+                                                               keys);
+  note_launch();
+  e = cudaGetLastError();
+  cudaFreeAsync(dgr, st);
+  return e;
+}
+
 }  // namespace corr

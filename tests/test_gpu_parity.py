@@ -232,3 +232,51 @@ def test_full_size_context_sampled_region_max(cfg, S, nreg):
             v = oracle.eval_pairs(mini, None, oracle.KSG, 3, [pos[got_arg[r][0]]], [pos[got_arg[r][1]]])[0]
             assert abs(v - ref_max[r]) <= 2 * KSG_TOL
     f.close()
+
+
+def _block_compare(f, fb, vals_a, vals_b, dims, A, B, absval=False):
+    measure = cb.CORR_PEARSON | (cb.CORR_F_ABS if absval else 0)
+    got_max, got_arg = cb.corr_region_max(f, fb, measure, 0, A, B, 0, 0)
+    cb.corr_check(f)
+    got_max, got_arg = _cpu(got_max), _cpu(got_arg)
+    for r in range(len(A)):
+        v, ab = oracle.pearson_block_max(vals_a, vals_b, dims, A[r], B[r], absval=absval)
+        assert abs(got_max[r] - v) <= PEARSON_TOL, (r, got_max[r], v)
+        if tuple(got_arg[r]) != ab:
+            w = oracle.eval_pairs(vals_a, vals_b, oracle.PEARSON, 0, [got_arg[r][0]], [got_arg[r][1]])[0]
+            w = abs(w) if absval else w
+            assert abs(w - v) <= 2 * PEARSON_TOL, (r, got_arg[r], ab, w, v)
+
+
+def test_pearson_block_c2_focus_full():
+    """C2: all 20 480^2 = 4.2e8 point pairs of the two focus bricks, n = 100, tcgen05 path."""
+    spec = synth.spec_of(synth.C2)
+    vals, f = _field(spec)
+    host = vals.cpu().numpy()
+    _block_compare(f, None, host, None, (spec.nx, spec.ny, spec.nz), [synth.C2_REGION_A], [synth.C2_REGION_B])
+    got_max, _ = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, [synth.C2_REGION_A], [synth.C2_REGION_B], 0, 0)
+    assert abs(float(got_max[0]) - 1.0) <= 1e-6  # cluster centres share one signal (PAPER.md:538)
+
+
+def test_pearson_block_context_boundary_and_overlap():
+    spec = synth.spec_of(synth.C3)
+    vals, f = _field(spec)
+    host = vals.cpu().numpy()
+    bricks = synth.bricks_of(synth.C3)
+    A = [bricks[7], bricks[0], bricks[15], bricks[40], (100, 100, 3, 164, 110, 9)]
+    B = [bricks[80], bricks[87], bricks[16], bricks[40], (120, 96, 0, 150, 140, 20)]
+    _block_compare(f, None, host, None, (spec.nx, spec.ny, spec.nz), A, B)
+    _block_compare(f, None, host, None, (spec.nx, spec.ny, spec.nz), A[:3], B[:3], absval=True)
+
+
+def test_pearson_block_n1000_and_two_fields():
+    cfg = synth.C5
+    sa, sb = synth.spec_of(cfg, 1), synth.spec_of(cfg, 2)
+    va, fa = _field(sa)
+    vb, fb = _field(sb)
+    ha, hb = va.cpu().numpy(), vb.cpu().numpy()
+    del va, vb
+    A = [(8, 8, 5, 40, 16, 10), (160, 232, 8, 192, 248, 12)]
+    B = [(170, 230, 8, 202, 238, 13), (0, 0, 0, 16, 16, 5)]
+    _block_compare(fa, fb, ha, hb, (sa.nx, sa.ny, sa.nz), A, B)
+    _block_compare(fa, None, ha, None, (sa.nx, sa.ny, sa.nz), A, B)

@@ -119,3 +119,28 @@ def test_cluster_centres_pearson_max_is_one():
     assert abs(mx[0] - 1.0) < 1e-6
     pb = (c1.z * 8 + c1.y) * 8 + c1.x
     assert arg[0][1] == pb
+
+
+@pytest.mark.parametrize("absval", [False, True])
+def test_pearson_block_max_matmul_equals_brute_force(absval):
+    """The oracle's library-matmul block max (used at full brick size) against the plain C
+    brute force over every pair (two independent implementations of PAPER.md:133/169)."""
+    spec, f = _c1_field()
+    boxes = synth.bricks_of(synth.C1)
+    A, B = synth.context_pairs(boxes)
+    A.append((0, 0, 0, 8, 8, 2))
+    B.append((0, 0, 0, 8, 8, 2))  # overlapping boxes: self pairs skipped
+    measure = oracle.PEARSON | (oracle.F_ABS if absval else 0)
+    mx, arg = oracle.region_max(f, None, (8, 8, 4), measure, 0, A, B, 0, 0)
+    for r in range(len(A)):
+        v, ab = oracle.pearson_block_max(f, None, (8, 8, 4), A[r], B[r], absval=absval, chunk=7)
+        assert abs(v - mx[r]) <= 1e-7
+        if v == mx[r]:
+            assert ab == tuple(arg[r])
+    spec2 = synth.spec_of(synth.C1, 2)
+    g = synth.generate(spec2).numpy()
+    A2, B2 = synth.matrix_pairs(boxes)
+    mx, arg = oracle.region_max(f, g, (8, 8, 4), oracle.PEARSON, 0, A2, B2, 0, 0)
+    for r in range(len(A2)):
+        v, ab = oracle.pearson_block_max(f, g, (8, 8, 4), A2[r], B2[r])
+        assert abs(v - mx[r]) <= 1e-7
