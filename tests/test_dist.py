@@ -1,0 +1,84 @@
+"""Multi-GPU host logic (dist.py) on CPU: world-size-2 gloo process groups.
+
+The shard -> all-gather path must reproduce the single-process result bit for bit
+(SURVEY.md §8(e)); the per-rank region maxima here come from the CPU oracle on
+each rank's shard (the GPU path's shard identity is a -m gpu test)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2309_03308_b200 import dist as cdist
+from paper_2309_03308_b200 import synth
+
+
+def test_shard_bounds_cover_and_balance():
+    for n, w in ((3828, 1), (3828, 2), (3828, 8), (7, 8), (10, 3)):
+        b = cdist.shard_bounds([1] * n, w)
+        assert b[0][0] == 0 and b[-1][1] == n and len(b) == w
+        assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
+        sizes = [hi - lo for lo, hi in b]
+        assert max(sizes) - min(sizes) <= 1
+    wts = [16640 * 20480 if i % 8 == 7 else 20480 * 20480 for i in range(88)]
+    b = cdist.shard_bounds(wts, 4)
+    loads = [sum(wts[lo:hi]) for lo, hi in b]
+    assert max(loads) / min(loads) < 1.1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    spec = synth.spec_of(synth.C1)
+    f = synth.generate(spec).numpy()
+    A, B = synth.context_pairs(synth.bricks_of(synth.C1))
+    bounds = cdist.shard_bounds([25] * len(A), world)
+    lo, hi = bounds[rank]
+    m, a = oracle.region_max(f, None, (8, 8, 4), oracle.KSG, 3, A[lo:hi], B[lo:hi], 25, 11)
+    fm, fa = cdist.gather_region_results(torch.from_numpy(m.astype(np.float32)), torch.from_numpy(a), bounds)
+    # focus: one region pair split into slabs of A
+    FA, FB = (0, 0, 0, 8, 8, 2), (0, 0, 2, 8, 8, 4)
+    slabs = cdist.split_box_z(FA, world)
+    sm, sa = oracle.region_max(f, None, (8, 8, 4), oracle.PEARSON, 0, [slabs[rank]], [FB], 0, 0)
+    parts = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+    tdist.all_gather(parts, torch.tensor([sm[0], sa[0][0], sa[0][1]], dtype=torch.float64))
+    v, ab = cdist.combine_focus([float(p[0]) for p in parts], [(int(p[1]), int(p[2])) for p in parts], slabs, FB, 8, 8)
+    q.put((rank, fm.numpy(), fa.numpy(), v, ab))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_shards_gather_bit_identical(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spec = synth.spec_of(synth.C1)
+    f = synth.generate(spec).numpy()
+    A, B = synth.context_pairs(synth.bricks_of(synth.C1))
+    m, a = oracle.region_max(f, None, (8, 8, 4), oracle.KSG, 3, A, B, 25, 11)
+    fm_ref, fa_ref = oracle.region_max(f, None, (8, 8, 4), oracle.PEARSON, 0, [(0, 0, 0, 8, 8, 2)],
+                                       [(0, 0, 2, 8, 8, 4)], 0, 0)
+    for rank, fm, fa, v, ab in res:
+        assert np.array_equal(fm, m.astype(np.float32))  # every rank holds the full result
+        assert np.array_equal(fa, a)
+        assert v == fm_ref[0] and tuple(ab) == tuple(fa_ref[0])

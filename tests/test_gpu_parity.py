@@ -280,3 +280,27 @@ def test_pearson_block_n1000_and_two_fields():
     B = [(170, 230, 8, 202, 238, 13), (0, 0, 0, 16, 16, 5)]
     _block_compare(fa, fb, ha, hb, (sa.nx, sa.ny, sa.nz), A, B)
     _block_compare(fa, None, ha, None, (sa.nx, sa.ny, sa.nz), A, B)
+
+
+def test_shards_bit_identical_to_unsharded():
+    """1-GPU emulation of the R-GPU split: shards run one after the
+    other and concatenated equal the unsharded call bit for bit (sampler keyed by boxes)."""
+    from paper_2309_03308_b200 import dist as cdist
+    spec = synth.spec_of(synth.C3)
+    vals, f = _field(spec)
+    del vals
+    A, B = synth.context_pairs(synth.bricks_of(synth.C3))
+    A, B = A[:400], B[:400]
+    for measure, S in ((cb.CORR_KSG, 64), (cb.CORR_PEARSON, 64), (cb.CORR_PEARSON, 0)):
+        if S == 0:
+            A2, B2 = A[:12], B[:12]
+        else:
+            A2, B2 = A, B
+        full_m, full_a = cb.corr_region_max(f, None, measure, 3, A2, B2, S, 99)
+        for world in (2, 3, 8):
+            ms, as_ = [], []
+            for lo, hi in cdist.shard_bounds([1] * len(A2), world):
+                m, a = cb.corr_region_max(f, None, measure, 3, A2[lo:hi], B2[lo:hi], S, 99)
+                ms.append(m)
+                as_.append(a)
+            assert torch.equal(torch.cat(ms), full_m) and torch.equal(torch.cat(as_), full_a)
