@@ -125,6 +125,12 @@ int corr_ksg_debug(const corr_field* fa, const corr_field* fb, int32_t k, const 
  * CUDA error, else CORR_OK. */
 int corr_check(const corr_field* f, void* cuda_stream);
 
+/* corr_ksg_comparisons -- KSG member-comparisons (d_ij evaluations) executed on
+ * `device` since the last reset; the exact sweep skips comparisons that provably cannot change
+ * any eps_i, so this is <= n(n-1) per pair.  Synchronises the device; reset != 0 zeroes the
+ * counter after reading.  Diagnostic for the roofline report (bench.py). */
+int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset);
+
 /* Number of CUDA kernels this library has launched in this process (diagnostic; bench.py
  * reports the launches inside its timed region as `gpu_launches`). */
 int64_t corr_launch_count(void);

@@ -23,7 +23,8 @@ CORR_F_ABS = 1 << 9
 CORR_OK, CORR_E_INVAL, CORR_E_RANGE, CORR_E_NOMEM, CORR_E_CUDA = 0, -1, -2, -3, -4
 
 EXPORTS = ("corr_field_create", "corr_field_destroy", "corr_field_info", "corr_eval_pairs",
-           "corr_region_max", "corr_ksg_debug", "corr_check", "corr_launch_count", "corr_last_error")
+           "corr_region_max", "corr_ksg_debug", "corr_check", "corr_ksg_comparisons", "corr_launch_count",
+           "corr_last_error")
 
 
 class CorrError(RuntimeError):
@@ -61,6 +62,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     L.corr_ksg_debug.argtypes = [vp, vp, i32, vp, vp, i64, vp, vp, vp, vp]
     L.corr_check.argtypes = [vp, vp]
     L.corr_launch_count.argtypes = []
+    L.corr_ksg_comparisons.argtypes = [i32, ctypes.POINTER(i64), i32]
     L.corr_last_error.restype = ctypes.c_char_p
     L.corr_last_error.argtypes = []
     for name in EXPORTS[:-2]:
@@ -193,6 +195,12 @@ def corr_ksg_debug(fa: Field, fb: Optional[Field], k: int, idxA: torch.Tensor, i
                                  ctypes.c_void_p(_ptr(nx)), ctypes.c_void_p(_ptr(ny)),
                                  ctypes.c_void_p(_stream(stream))))
     return eps, nx, ny
+
+
+def corr_ksg_comparisons(device: int = 0, reset: bool = True) -> int:
+    v = ctypes.c_int64()
+    _check(load().corr_ksg_comparisons(device, ctypes.byref(v), int(reset)))
+    return v.value
 
 
 def corr_launch_count() -> int:

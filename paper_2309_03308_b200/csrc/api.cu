@@ -55,6 +55,7 @@ void free_field(corr_field* f) {
   cudaFree(f->S);
   cudaFree(f->perm);
   cudaFree(f->cflag);
+  cudaFree(f->spread);
   cudaFree(f->psi);
   cudaFree(f->err);
   cudaFree(f->tmaps);
@@ -111,6 +112,18 @@ const char* corr_last_error(void) { return g_last_error.c_str(); }
 
 int64_t corr_launch_count(void) { return (int64_t)g_launch_count.load(); }
 
+int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset) {
+  if (!count) return fail(CORR_E_INVAL, "count is NULL");
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long v = 0;
+  if (e == cudaSuccess) e = ksg_comparisons(&v, reset != 0);
+  if (e != cudaSuccess) return cuda_fail(e, "corr_ksg_comparisons");
+  *count = (int64_t)v;
+  return CORR_OK;
+}
+
 int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t device,
                       void* cuda_stream, corr_field** out) {
   if (!out) return fail(CORR_E_INVAL, "out is NULL");
@@ -146,7 +159,7 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
   if (!alloc((void**)&f->F, row_elems * 4) || !alloc((void**)&f->Z, row_elems * 4) ||
       !alloc((void**)&f->Zhi, row_elems * 4) || !alloc((void**)&f->Zlo, row_elems * 4) ||
       !alloc((void**)&f->S, row_elems * 4) || !alloc((void**)&f->perm, row_elems * 2) ||
-      !alloc((void**)&f->cflag, (size_t)f->P) || !alloc((void**)&f->psi, ((size_t)members + 2) * 8) ||
+      !alloc((void**)&f->cflag, (size_t)f->P) || !alloc((void**)&f->spread, (size_t)f->P * 4) || !alloc((void**)&f->psi, ((size_t)members + 2) * 8) ||
       !alloc((void**)&f->err, sizeof(int))) {
     free_field(f);
     return fail(CORR_E_NOMEM, "device allocation failed for the field");

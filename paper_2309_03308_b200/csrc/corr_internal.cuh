@@ -21,6 +21,7 @@ struct corr_field {
   float* S;       // [P][n_pad] row sorted ascending, pad = +inf
   uint16_t* perm; // [P][n_pad] argsort of the row (S[p][t] = F[p][perm[p][t]])
   uint8_t* cflag; // [P] 1 = constant series (min == max)
+  float* spread;  // [P] ||x - mean|| (picks the sort marginal of a KSG pair)
   double* psi;    // [n + 2] digamma at integers, psi[0] = NaN
   int* err;       // device status word: bit0 = index out of range, bit1 = non-finite input
   void* tmaps;    // lazily built TMA descriptors (pearson_gemm.cu)
@@ -71,6 +72,10 @@ struct PairOut {
 cudaError_t launch_field_ingest(corr_field* f, const float* dvalues_member_major, cudaStream_t st);
 cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1,
                        const PairSrc& src, const PairOut& out, cudaStream_t st);
+// n > 128 members: x-sorted / filtered / sweep kernel (ksg_sorted.cu)
+cudaError_t launch_ksg_sorted(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
+                              const PairOut& out, cudaStream_t st);
+cudaError_t ksg_comparisons(unsigned long long* value, bool reset);
 cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
                                  const PairOut& out, cudaStream_t st);
 cudaError_t launch_region_finalize(const PairSrc& src, const unsigned long long* keys,

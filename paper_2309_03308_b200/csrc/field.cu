@@ -62,8 +62,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 // ---- 2. per-point statistics, standardisation, tf32 split (one warp per row) ---
 __global__ void __launch_bounds__(256) stats_kernel(const float* __restrict__ F, float* __restrict__ Z,
                                                     float* __restrict__ Zhi, float* __restrict__ Zlo,
-                                                    uint8_t* __restrict__ cflag, int n, int n_pad,
-                                                    int64_t P) {
+                                                    uint8_t* __restrict__ cflag, float* __restrict__ spread,
+                                                    int n, int n_pad, int64_t P) {
   const int lane = threadIdx.x & 31;
   const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= P) return;
@@ -100,7 +100,10 @@ __global__ void __launch_bounds__(256) stats_kernel(const float* __restrict__ F,
     Zhi[p * n_pad + e] = hi;
     Zlo[p * n_pad + e] = lo;
   }
-  if (lane == 0) cflag[p] = constant ? 1 : 0;
+  if (lane == 0) {
+    cflag[p] = constant ? 1 : 0;
+    spread[p] = constant ? 0.f : (float)sqrt(ss);
+  }
 }
 
 // ---- 3. per-row bitonic sort with argsort (shared memory) ----------------------
@@ -157,7 +160,7 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
   {
     const int64_t threads = P * 32;
     stats_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(f->F, f->Z, f->Zhi, f->Zlo, f->cflag,
-                                                                   f->n, f->n_pad, P);
+                                                                   f->spread, f->n, f->n_pad, P);
   }
   {
     int log2n2 = 1;

@@ -28,15 +28,6 @@ namespace {
 constexpr int R = 4;            // members per lane
 constexpr int kBlockMembers = 32 * R;
 
-// CORR_KSG_SWEEP=1 in the environment enables the early-terminating sweep (NEXT #1).
-bool ksg_sweep_enabled() {
-  static const int v = [] {
-    const char* s = getenv("CORR_KSG_SWEEP");
-    return (s && s[0] == '1') ? 1 : 0;
-  }();
-  return v != 0;
-}
-
 __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
   unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a);
   unsigned long long ub = *reinterpret_cast<unsigned long long*>(&b);
@@ -241,291 +232,10 @@ __global__ void __launch_bounds__(256) ksg_kernel(const float* __restrict__ Fa, 
   }
 }
 
-// ============================================================================
-// v1 (n > 128): x-sorted members, outward j-order, filtered insertion.
-//
-// ncu on v0 (profiles/r01_ksg_v0_ncu.txt): the ALU pipe (FMNMX) is 89% busy at IPC
-// 2.27 -- FMNMX issues at 0.5/clk/SMSP on B200, and the 2k-1 FMNMX network per
-// comparison is the bound.  v1 makes the network rare instead of cheaper:
-//  * the pair is staged in the x-sorted order of series a (field argsort):
-//    xy[t] = (S_a[t], F_b[perm_a[t]]) -- a member permutation, so eps and the counts
-//    are unchanged (the k-th order statistic is order-free; reading R4);
-//  * a warp owns 128 x-consecutive members and scans the j's of its own block first,
-//    then 32-wide chunks outward (alternating below/above), so each list converges to
-//    its final k-th distance after a few chunks;
-//  * per group of 4 j's and member the kernel computes the 4 distances (FADD2 +
-//    FMNMX|.|), their min (FMNMX3 + FMNMX) and one compare against the list's k-th
-//    entry; only if some lane of the warp can insert (VOTE.ANY) does the warp run the
-//    exact merge network (min over i+j=r of max(l_i, y_j), 3k-1 FMNMX per 2 values).
-//    Inserting a d >= l[K-1] is a no-op, so skipping the network is exact.
-// SWEEP (NEXT #1 of SURVEY.md §8(f)): stop scanning in a direction once the x-gap
-// fl(x_block_edge - x_chunk_edge) is >= every member's current k-th distance --
-// exact because |fl(x_i - x_j)| >= that gap for every remaining j (monotone rounding).
-// ============================================================================
-template <int K>
-__device__ __forceinline__ void merge2(float (&l)[K], float d0, float d1) {
-  const float a = fminf(d0, d1), b = fmaxf(d0, d1);
-  float nl[K];
-  nl[0] = fminf(l[0], a);
-  if (K >= 2) nl[1] = fminf(fminf(l[1], fmaxf(l[0], a)), b);
-#pragma unroll
-  for (int r = 2; r < K; ++r) nl[r] = fminf(fminf(l[r], fmaxf(l[r - 1], a)), fmaxf(l[r - 2], b));
-#pragma unroll
-  for (int r = 0; r < K; ++r) l[r] = nl[r];
-}
-
-__device__ __forceinline__ float cheb(float2 zi, float2 zj) {
-  const float2 d = sub2(zi, zj);
-  return fmaxf(fabsf(d.x), fabsf(d.y));
-}
-
-// strict marginal count on a strided sorted array (see marginal_count)
-__device__ __forceinline__ int marginal_count_strided(const float* __restrict__ S, int stride, int n, float v,
-                                                      float e) {
-  int lo = 0, len = n;
-  while (len > 0) {
-    const int half = len >> 1;
-    const float s = S[(lo + half) * stride];
-    const bool pred = (s >= v) && (s - v >= e);
-    if (pred) len = half; else { lo += half + 1; len -= half + 1; }
-  }
-  const int u = lo;
-  lo = 0; len = n;
-  while (len > 0) {
-    const int half = len >> 1;
-    const float s = S[(lo + half) * stride];
-    const bool pred = (s >= v) || (v - s < e);
-    if (pred) len = half; else { lo += half + 1; len -= half + 1; }
-  }
-  return (u - lo) - (e > 0.f ? 1 : 0);
-}
-
-// One filtered 32-j chunk for the R members of this lane.
-template <int K, bool DESC>
-__device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[R],
-                                               float (&l)[R][K]) {
-#pragma unroll 2
-  for (int gi = 0; gi < 8; ++gi) {
-    const int g = DESC ? 7 - gi : gi;
-    const float4 v0 = cp[2 * g], v1 = cp[2 * g + 1];
-    const float2 z0 = make_float2(v0.x, v0.y), z1 = make_float2(v0.z, v0.w);
-    const float2 z2 = make_float2(v1.x, v1.y), z3 = make_float2(v1.z, v1.w);
-    float d[R][4];
-    bool p = false;
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) {
-      d[rr][0] = cheb(zi[rr], z0);
-      d[rr][1] = cheb(zi[rr], z1);
-      d[rr][2] = cheb(zi[rr], z2);
-      d[rr][3] = cheb(zi[rr], z3);
-      const float m = fminf(fminf(fminf(d[rr][0], d[rr][1]), d[rr][2]), d[rr][3]);
-      p |= m < l[rr][K - 1];
-    }
-    if (__any_sync(0xffffffffu, p)) {
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        merge2<K>(l[rr], d[rr][0], d[rr][1]);
-        merge2<K>(l[rr], d[rr][2], d[rr][3]);
-      }
-    }
-  }
-}
-
-template <int K, bool SWEEP>
-__global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
-    const float* __restrict__ Sa, const uint16_t* __restrict__ perm_a, const float* __restrict__ Fb,
-    const float* __restrict__ Sb, const uint8_t* __restrict__ ca, const uint8_t* __restrict__ cb,
-    const double* __restrict__ psi_g, int n, int n_pad, int k, int plus1, PairSrc src, PairOut out) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  const int nthreads = blockDim.x;
-  const int nblk = (n + kBlockMembers - 1) / kBlockMembers;
-  const int nxy = nblk * kBlockMembers;
-  const int nch = (n + 31) >> 5;
-
-  double* psi = reinterpret_cast<double*>(smem_raw);
-  const int psi_len = (n + 2 + 1) & ~1;
-  float2* xy = reinterpret_cast<float2*>(smem_raw + psi_len * sizeof(double));
-  float* sy = reinterpret_cast<float*>(xy + nxy);
-  float* tb = sy + n_pad;
-  uint16_t* pm = reinterpret_cast<uint16_t*>(tb + n_pad);
-  double* red = reinterpret_cast<double*>(pm + n_pad + 8);  // n_pad % 8 == 0 -> 16-byte aligned
-
-  for (int i = threadIdx.x; i < n + 2; i += nthreads) psi[i] = psi_g[i];
-  __syncthreads();
-  const double psi_nk = psi[n] + psi[k];
-  const int off = plus1 ? 1 : 0;
-
-  for (int64_t u = blockIdx.x; u < src.nunits; u += gridDim.x) {
-    int64_t a, b, r;
-    uint32_t idx;
-    const bool ok = unit_pair(src, u, a, b, r, idx);
-    if (!ok) {
-      if (src.mode == kList && threadIdx.x == 0) out.out[u] = NAN;
-      continue;
-    }
-    const bool degenerate = (ca[a] | cb[b]) != 0;
-    if (degenerate && out.dbg_eps == nullptr) {
-      if (src.mode == kList && threadIdx.x == 0) out.out[u] = NAN;
-      continue;
-    }
-    __syncthreads();
-    // ---- a2: stage (F_b row, sorted rows, argsort of a) ----
-    {
-      const float4* fb4 = reinterpret_cast<const float4*>(Fb + b * n_pad);
-      const float4* sb4 = reinterpret_cast<const float4*>(Sb + b * n_pad);
-      const uint2* pa2 = reinterpret_cast<const uint2*>(perm_a + a * n_pad);
-      for (int q = threadIdx.x; q < n_pad / 4; q += nthreads) {
-        reinterpret_cast<float4*>(tb)[q] = __ldg(fb4 + q);
-        reinterpret_cast<float4*>(sy)[q] = __ldg(sb4 + q);
-        reinterpret_cast<uint2*>(pm)[q] = __ldg(pa2 + q);
-      }
-    }
-    __syncthreads();
-    {
-      const float4* sa4 = reinterpret_cast<const float4*>(Sa + a * n_pad);
-      for (int q = threadIdx.x; q < nxy / 4; q += nthreads) {
-        const int t = 4 * q;
-        float4 xs = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-        if (t < n_pad) xs = __ldg(sa4 + q);
-        float4* dst = reinterpret_cast<float4*>(xy + t);
-        const float inf = INFINITY;
-        dst[0] = make_float4(t + 0 < n ? xs.x : inf, t + 0 < n ? tb[pm[t + 0]] : inf,
-                             t + 1 < n ? xs.y : inf, t + 1 < n ? tb[pm[t + 1]] : inf);
-        dst[1] = make_float4(t + 2 < n ? xs.z : inf, t + 2 < n ? tb[pm[t + 2]] : inf,
-                             t + 3 < n ? xs.w : inf, t + 3 < n ? tb[pm[t + 3]] : inf);
-      }
-    }
-    __syncthreads();
-
-    // ---- a3 / a4 / a5 ----
-    const float4* xy4 = reinterpret_cast<const float4*>(xy);
-    double acc = 0.0;
-    for (int mb = warp; mb < nblk; mb += nwarps) {
-      float2 zi[R];
-      float l[R][K];
-      int ts[R];
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        ts[rr] = mb * kBlockMembers + 32 * rr + lane;
-        zi[rr] = xy[ts[rr]];
-#pragma unroll
-        for (int t = 0; t < K; ++t) l[rr][t] = INFINITY;
-      }
-      // own block (contains the self pairs): exact network with the j == i mask
-      const int c0 = 4 * mb, c1 = min(c0 + 4, nch);
-      for (int c = c0; c < c1; ++c) {
-        const float4* cp = xy4 + c * 16;
-        const int jb = c * 32;
-#pragma unroll 4
-        for (int h = 0; h < 16; ++h) {
-          const float4 v = cp[h];
-          const float2 z0 = make_float2(v.x, v.y), z1 = make_float2(v.z, v.w);
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) {
-            float e0 = cheb(zi[rr], z0), e1 = cheb(zi[rr], z1);
-            if (jb + 2 * h == ts[rr]) e0 = INFINITY;
-            if (jb + 2 * h + 1 == ts[rr]) e1 = INFINITY;
-            merge2<K>(l[rr], e0, e1);
-          }
-        }
-      }
-      // outward chunks
-      int clo = c0 - 1, chi = c1;
-      const float xblk_lo = xy[mb * kBlockMembers].x;
-      const float xblk_hi = xy[min(n, (mb + 1) * kBlockMembers) - 1].x;
-      while (clo >= 0 || chi < nch) {
-        float tmax = 0.f;
-        if (SWEEP) {
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr)
-            if (ts[rr] < n) tmax = fmaxf(tmax, l[rr][K - 1]);
-          tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
-        }
-        if (clo >= 0) {
-          if (SWEEP && (xblk_lo - xy[clo * 32 + 31].x) >= tmax) {
-            clo = -1;
-          } else {
-            chunk_filtered<K, true>(xy4 + clo * 16, zi, l);
-            --clo;
-          }
-        }
-        if (chi < nch) {
-          if (SWEEP && (xy[chi * 32].x - xblk_hi) >= tmax) {
-            chi = nch;
-          } else {
-            chunk_filtered<K, false>(xy4 + chi * 16, zi, l);
-            ++chi;
-          }
-        }
-      }
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        if (ts[rr] < n) {
-          const float e = l[rr][K - 1];
-          const int cx = marginal_count_strided(reinterpret_cast<const float*>(xy), 2, n, zi[rr].x, e);
-          const int cy = marginal_count(sy, n, zi[rr].y, e);
-          acc += psi[cx + off] + psi[cy + off];
-          if (out.dbg_eps) {
-            const int m = pm[ts[rr]];
-            out.dbg_eps[u * n + m] = e;
-            out.dbg_nx[u * n + m] = cx;
-            out.dbg_ny[u * n + m] = cy;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) red[warp] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < nwarps; ++w) s += red[w];
-      const float mi = degenerate ? NAN : (float)(psi_nk - s / (double)n);
-      if (src.mode == kList) {
-        out.out[u] = mi;
-      } else if (!isnan(mi)) {
-        atomicMax(out.keys + r, pack_key(out.absval ? fabsf(mi) : mi, idx));
-      }
-    }
-  }
-}
-
-template <int K, bool SWEEP>
-cudaError_t launch_sorted(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
-                          const PairOut& out, cudaStream_t st) {
-  const int n = fa->n, n_pad = fa->n_pad;
-  const int nblk = (n + kBlockMembers - 1) / kBlockMembers;
-  const int nxy = nblk * kBlockMembers;
-  const size_t smem = (size_t)((n + 2 + 1) & ~1) * sizeof(double) + (size_t)nxy * sizeof(float2) +
-                      2 * (size_t)n_pad * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
-                      32 * sizeof(double);
-  auto kern = ksg_sorted_kernel<K, SWEEP>;
-  const int warps = nblk < 8 ? nblk : 8;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);
-  if (occ < 1) occ = 1;
-  int64_t blocks = src.nunits;
-  const int64_t cap = (int64_t)kSMs * occ;
-  if (blocks > cap) blocks = cap;
-  kern<<<(unsigned)blocks, warps * 32, smem, st>>>(fa->S, fa->perm, fb->F, fb->S, fa->cflag, fb->cflag, fa->psi, n,
-                                                   n_pad, k, plus1, src, out);
-  note_launch();
-  return cudaGetLastError();
-}
-
 template <int K>
 cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                      const PairOut& out, cudaStream_t st) {
-  if (fa->n > kBlockMembers) {
-    if (ksg_sweep_enabled()) return launch_sorted<K, true>(fa, fb, k, plus1, src, out, st);
-    return launch_sorted<K, false>(fa, fb, k, plus1, src, out, st);
-  }
+  if (fa->n > kBlockMembers) return launch_ksg_sorted(fa, fb, k, plus1, src, out, st);
   const int n = fa->n, n_pad = fa->n_pad;
   const int nblk = (n + kBlockMembers - 1) / kBlockMembers;
   const int nxy = nblk * kBlockMembers;

@@ -1,0 +1,385 @@
+// ksg_sorted.cu -- KSG MI for n > 128 members: x-sorted, filtered, exact sweep.
+// SURVEY.md §8(a) rows a2-a5 (+ a8/a9 via the pair source); NEXT #1 of §8(f).
+//
+// Definitions (readings R1-R7): eps_i = k-th smallest Chebyshev distance
+// (fp32), strict marginal counts, MI = psi(n) + psi(k) - (1/n) sum_i [psi(n_x,i) + psi(n_y,i)].
+//
+// Measured facts that shape this kernel: FMNMX/FSETP issue on the ALU pipe at
+// 0.5 warp-instr/clk/SMSP (ncu: ALU 89 % busy at IPC 2.27 for the plain register network);
+// FMNMX3 costs the same slot for twice the work; FADD2 runs on the FMA pipe.  So the kernel
+// minimises ALU work per comparison:
+//  * the pair is staged sorted along its WIDER marginal (spread = ||x - mean||): the k-NN of a
+//    member then lies in a narrow window of that order.  KSG is symmetric in (x, y) (Eq. 1), so
+//    swapping the roles of a and b leaves eps unchanged and swaps the two counts (exact);
+//  * xy[t] = (S_u[t], F_v[perm_u[t]]) -- a member permutation; eps is order-free (R4);
+//  * a warp owns 32*RM sort-consecutive members (RM per lane: one broadcast LDS.128 of two
+//    joint samples feeds 2*RM comparisons); it scans its own block first (exact merge network,
+//    the j == i mask only on the diagonal member of each chunk), then 32-wide chunks outward;
+//  * outside the own block, per group of 4 j and member: 4 distances (FADD2 + FMNMX|.|), their
+//    min (FMNMX3 + FMNMX) and one compare with the list's k-th entry; only if some lane can
+//    insert (VOTE.ANY) does the warp run the exact merge network
+//        l'_r = min(l_r, max(l_{r-1}, a), max(l_{r-2}, b)),  (a, b) = sorted pair of new values
+//    -- inserting d >= l[K-1] is a no-op, so skipping it is exact;
+//  * SWEEP: a direction stops once fl(x_block_edge - x_chunk_edge) >= every member's current
+//    k-th distance: |fl(x_i - x_j)| >= that gap for all remaining j (monotone rounding), so no
+//    remaining j can enter any list (exact).  Executed comparisons are counted for the roofline;
+//  * counts: two binary searches per marginal on the sorted rows with monotone fp32
+//    predicates (bit-exact), psi from an fp64 shared table, fixed-order fp64 reduction.
+#include <math.h>
+#include <stdlib.h>
+
+#include "sampler.cuh"
+
+namespace corr {
+
+__device__ unsigned long long g_ksg_comparisons;  // executed comparisons (corr_ksg_comparisons)
+
+namespace {
+
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a);
+  unsigned long long ub = *reinterpret_cast<unsigned long long*>(&b);
+  unsigned long long ud;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ud) : "l"(ua), "l"(ub));
+  return *reinterpret_cast<float2*>(&ud);
+}
+
+__device__ __forceinline__ float cheb(float2 zi, float2 zj) {
+  const float2 d = sub2(zi, zj);
+  return fmaxf(fabsf(d.x), fabsf(d.y));
+}
+
+template <int K>
+__device__ __forceinline__ void merge2(float (&l)[K], float d0, float d1) {
+  const float a = fminf(d0, d1), b = fmaxf(d0, d1);
+  float nl[K];
+  nl[0] = fminf(l[0], a);
+  if (K >= 2) nl[1] = fminf(fminf(l[1], fmaxf(l[0], a)), b);
+#pragma unroll
+  for (int r = 2; r < K; ++r) nl[r] = fminf(fminf(l[r], fmaxf(l[r - 1], a)), fmaxf(l[r - 2], b));
+#pragma unroll
+  for (int r = 0; r < K; ++r) l[r] = nl[r];
+}
+
+// strict marginal count on a sorted array with element stride `st`:
+//   u = first s >= v with fl(s - v) >= e;  w = first s with s >= v or fl(v - s) < e
+//   count = (u - w) - [e > 0]        (the member itself lies in [w, u) iff e > 0)
+__device__ __forceinline__ int marginal_count(const float* __restrict__ S, int st, int n, float v, float e) {
+  int lo = 0, len = n;
+  while (len > 0) {
+    const int half = len >> 1;
+    const float s = S[(lo + half) * st];
+    if ((s >= v) && (s - v >= e)) len = half; else { lo += half + 1; len -= half + 1; }
+  }
+  const int u = lo;
+  lo = 0; len = n;
+  while (len > 0) {
+    const int half = len >> 1;
+    const float s = S[(lo + half) * st];
+    if ((s >= v) || (v - s < e)) len = half; else { lo += half + 1; len -= half + 1; }
+  }
+  return (u - lo) - (e > 0.f ? 1 : 0);
+}
+
+// own-block chunk: exact network; the self pair j == i exists only for member RC of each lane
+template <int K, int RM, int RC>
+__device__ __forceinline__ void own_chunk(const float4* __restrict__ cp, const float2 (&zi)[RM],
+                                          float (&l)[RM][K], int lane) {
+#pragma unroll 4
+  for (int h = 0; h < 16; ++h) {
+    const float4 v = cp[h];
+    const float2 z0 = make_float2(v.x, v.y), z1 = make_float2(v.z, v.w);
+#pragma unroll
+    for (int rr = 0; rr < RM; ++rr) {
+      float e0 = cheb(zi[rr], z0), e1 = cheb(zi[rr], z1);
+      if (rr == RC) {
+        if (2 * h == lane) e0 = INFINITY;
+        if (2 * h + 1 == lane) e1 = INFINITY;
+      }
+      merge2<K>(l[rr], e0, e1);
+    }
+  }
+}
+
+template <int K, int RM, int RC>
+struct OwnBlock {
+  __device__ __forceinline__ static void run(const float4* xy4, int c0, int nch, const float2 (&zi)[RM],
+                                             float (&l)[RM][K], int lane) {
+    OwnBlock<K, RM, RC - 1>::run(xy4, c0, nch, zi, l, lane);
+    if (c0 + RC < nch) own_chunk<K, RM, RC>(xy4 + (c0 + RC) * 16, zi, l, lane);
+  }
+};
+template <int K, int RM>
+struct OwnBlock<K, RM, -1> {
+  __device__ __forceinline__ static void run(const float4*, int, int, const float2 (&)[RM], float (&)[RM][K], int) {}
+};
+
+// one filtered 32-j chunk
+template <int K, int RM, bool DESC>
+__device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
+                                               float (&l)[RM][K]) {
+#pragma unroll 2
+  for (int gi = 0; gi < 8; ++gi) {
+    const int g = DESC ? 7 - gi : gi;
+    const float4 v0 = cp[2 * g], v1 = cp[2 * g + 1];
+    const float2 z0 = make_float2(v0.x, v0.y), z1 = make_float2(v0.z, v0.w);
+    const float2 z2 = make_float2(v1.x, v1.y), z3 = make_float2(v1.z, v1.w);
+    float d[RM][4];
+    bool p = false;
+#pragma unroll
+    for (int rr = 0; rr < RM; ++rr) {
+      d[rr][0] = cheb(zi[rr], z0);
+      d[rr][1] = cheb(zi[rr], z1);
+      d[rr][2] = cheb(zi[rr], z2);
+      d[rr][3] = cheb(zi[rr], z3);
+      const float m = fminf(fminf(fminf(d[rr][0], d[rr][1]), d[rr][2]), d[rr][3]);
+      p |= m < l[rr][K - 1];
+    }
+    if (__any_sync(0xffffffffu, p)) {
+#pragma unroll
+      for (int rr = 0; rr < RM; ++rr) {
+        merge2<K>(l[rr], d[rr][0], d[rr][1]);
+        merge2<K>(l[rr], d[rr][2], d[rr][3]);
+      }
+    }
+  }
+}
+
+template <int K, int RM, bool SWEEP>
+__global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
+    const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
+    const float* __restrict__ Sb, const uint16_t* __restrict__ Pb, const float* __restrict__ Fb,
+    const float* __restrict__ spa, const float* __restrict__ spb, const uint8_t* __restrict__ ca,
+    const uint8_t* __restrict__ cb, const double* __restrict__ psi_g, int n, int n_pad, int k, int plus1,
+    PairSrc src, PairOut out) {
+  constexpr int BLK = 32 * RM;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int nthreads = blockDim.x;
+  const int nblk = (n + BLK - 1) / BLK;
+  const int nxy = ((n + 127) / 128) * 128;
+  const int nch = (n + 31) >> 5;
+
+  double* psi = reinterpret_cast<double*>(smem_raw);
+  const int psi_len = (n + 2 + 1) & ~1;
+  float2* xy = reinterpret_cast<float2*>(smem_raw + psi_len * sizeof(double));
+  float* sy = reinterpret_cast<float*>(xy + nxy);
+  float* tb = sy + n_pad;
+  uint16_t* pm = reinterpret_cast<uint16_t*>(tb + n_pad);
+  double* red = reinterpret_cast<double*>(pm + n_pad + 8);
+  int* next_blk = reinterpret_cast<int*>(red + 32);
+
+  for (int i = threadIdx.x; i < n + 2; i += nthreads) psi[i] = psi_g[i];
+  __syncthreads();
+  const double psi_nk = psi[n] + psi[k];
+  const int off = plus1 ? 1 : 0;
+  unsigned long long executed = 0;
+
+  for (int64_t u = blockIdx.x; u < src.nunits; u += gridDim.x) {
+    int64_t a, b, r;
+    uint32_t idx;
+    const bool ok = unit_pair(src, u, a, b, r, idx);
+    if (!ok) {
+      if (src.mode == kList && threadIdx.x == 0) out.out[u] = NAN;
+      continue;
+    }
+    const bool degenerate = (ca[a] | cb[b]) != 0;
+    if (degenerate && out.dbg_eps == nullptr) {
+      if (src.mode == kList && threadIdx.x == 0) out.out[u] = NAN;
+      continue;
+    }
+    // sort along the wider marginal (swap roles of x and y; exact by Eq. 1 symmetry)
+    const bool swap = spb[b] > spa[a];
+    const float* Su = swap ? Sb + b * n_pad : Sa + a * n_pad;
+    const uint16_t* Pu = swap ? Pb + b * n_pad : Pa + a * n_pad;
+    const float* Fv = swap ? Fa + a * n_pad : Fb + b * n_pad;
+    const float* Sv = swap ? Sa + a * n_pad : Sb + b * n_pad;
+    __syncthreads();
+    if (threadIdx.x == 0) *next_blk = nwarps;  // blocks 0..nwarps-1 are taken statically
+    // ---- a2: stage ----
+    for (int q = threadIdx.x; q < n_pad / 4; q += nthreads) {
+      reinterpret_cast<float4*>(tb)[q] = __ldg(reinterpret_cast<const float4*>(Fv) + q);
+      reinterpret_cast<float4*>(sy)[q] = __ldg(reinterpret_cast<const float4*>(Sv) + q);
+      reinterpret_cast<uint2*>(pm)[q] = __ldg(reinterpret_cast<const uint2*>(Pu) + q);
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nxy / 4; q += nthreads) {
+      const int t = 4 * q;
+      float4 xs = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+      if (t < n_pad) xs = __ldg(reinterpret_cast<const float4*>(Su) + q);
+      float4* dst = reinterpret_cast<float4*>(xy + t);
+      const float inf = INFINITY;
+      dst[0] = make_float4(t + 0 < n ? xs.x : inf, t + 0 < n ? tb[pm[t + 0]] : inf, t + 1 < n ? xs.y : inf,
+                           t + 1 < n ? tb[pm[t + 1]] : inf);
+      dst[1] = make_float4(t + 2 < n ? xs.z : inf, t + 2 < n ? tb[pm[t + 2]] : inf, t + 3 < n ? xs.w : inf,
+                           t + 3 < n ? tb[pm[t + 3]] : inf);
+    }
+    __syncthreads();
+
+    // ---- a3 / a4 / a5 ----
+    const float4* xy4 = reinterpret_cast<const float4*>(xy);
+    double acc = 0.0;
+    // member blocks: first one static, then dynamic (sweep lengths differ per block)
+    for (int mb = warp; mb < nblk;) {
+      float2 zi[RM];
+      float l[RM][K];
+      int ts[RM];
+#pragma unroll
+      for (int rr = 0; rr < RM; ++rr) {
+        ts[rr] = mb * BLK + 32 * rr + lane;
+        zi[rr] = xy[ts[rr]];
+#pragma unroll
+        for (int t = 0; t < K; ++t) l[rr][t] = INFINITY;
+      }
+      const int c0 = mb * RM;
+      const int c1 = min(c0 + RM, nch);
+      OwnBlock<K, RM, RM - 1>::run(xy4, c0, nch, zi, l, lane);
+      int nproc = c1 - c0;
+      int clo = c0 - 1, chi = c1;
+      const float xblk_lo = xy[mb * BLK].x;
+      const float xblk_hi = xy[min(n, (mb + 1) * BLK) - 1].x;
+      while (clo >= 0 || chi < nch) {
+        float tmax = 0.f;
+        if (SWEEP) {
+#pragma unroll
+          for (int rr = 0; rr < RM; ++rr)
+            if (ts[rr] < n) tmax = fmaxf(tmax, l[rr][K - 1]);
+          tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+        }
+        if (clo >= 0) {
+          if (SWEEP && (xblk_lo - xy[clo * 32 + 31].x) >= tmax) {
+            clo = -1;
+          } else {
+            chunk_filtered<K, RM, true>(xy4 + clo * 16, zi, l);
+            --clo;
+            ++nproc;
+          }
+        }
+        if (chi < nch) {
+          if (SWEEP && (xy[chi * 32].x - xblk_hi) >= tmax) {
+            chi = nch;
+          } else {
+            chunk_filtered<K, RM, false>(xy4 + chi * 16, zi, l);
+            ++chi;
+            ++nproc;
+          }
+        }
+      }
+      const int valid = min(BLK, n - mb * BLK);
+      if (lane == 0) executed += (unsigned long long)nproc * 32ull * (unsigned long long)valid;
+#pragma unroll
+      for (int rr = 0; rr < RM; ++rr) {
+        if (ts[rr] < n) {
+          const float e = l[rr][K - 1];
+          const int cu = marginal_count(reinterpret_cast<const float*>(xy), 2, n, zi[rr].x, e);
+          const int cv = marginal_count(sy, 1, n, zi[rr].y, e);
+          acc += psi[cu + off] + psi[cv + off];
+          if (out.dbg_eps) {
+            const int m = pm[ts[rr]];
+            out.dbg_eps[u * n + m] = e;
+            out.dbg_nx[u * n + m] = swap ? cv : cu;
+            out.dbg_ny[u * n + m] = swap ? cu : cv;
+          }
+        }
+      }
+      int nb = 0;
+      if (lane == 0) nb = atomicAdd(next_blk, 1);
+      mb = __shfl_sync(0xffffffffu, nb, 0);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < nwarps; ++w) s += red[w];
+      const float mi = degenerate ? NAN : (float)(psi_nk - s / (double)n);
+      if (src.mode == kList) {
+        out.out[u] = mi;
+      } else if (!isnan(mi)) {
+        atomicMax(out.keys + r, pack_key(out.absval ? fabsf(mi) : mi, idx));
+      }
+    }
+  }
+  if (lane == 0 && executed) atomicAdd(&g_ksg_comparisons, executed);
+}
+
+template <int K, int RM, bool SWEEP>
+cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
+                     const PairOut& out, cudaStream_t st) {
+  const int n = fa->n, n_pad = fa->n_pad;
+  const int nxy = ((n + 127) / 128) * 128;
+  const int nblk = (n + 32 * RM - 1) / (32 * RM);
+  const size_t smem = (size_t)((n + 2 + 1) & ~1) * sizeof(double) + (size_t)nxy * sizeof(float2) +
+                      2 * (size_t)n_pad * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
+                      32 * sizeof(double) + 16;
+  auto kern = ksg_sorted_kernel<K, RM, SWEEP>;
+  const int warps = nblk < 8 ? nblk : 8;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);
+  if (occ < 1) occ = 1;
+  int64_t blocks = src.nunits;
+  const int64_t cap = (int64_t)kSMs * occ;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, warps * 32, smem, st>>>(fa->S, fa->perm, fa->F, fb->S, fb->perm, fb->F, fa->spread,
+                                                   fb->spread, fa->cflag, fb->cflag, fa->psi, n, n_pad, k, plus1,
+                                                   src, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s && *s ? atoi(s) : dflt;
+}
+
+template <int K>
+cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
+                     const PairOut& out, cudaStream_t st) {
+  // CORR_KSG_SWEEP=0 disables the exact sweep (dense n(n-1) comparisons); CORR_KSG_RM picks
+  // members per lane (1, 2 or 4).
+  static const int sweep = env_int("CORR_KSG_SWEEP", 1);
+  static const int rm = env_int("CORR_KSG_RM", 2);
+  if (rm == 4) {
+    return sweep ? launch_t<K, 4, true>(fa, fb, k, plus1, src, out, st)
+                 : launch_t<K, 4, false>(fa, fb, k, plus1, src, out, st);
+  }
+  if (rm == 1) {
+    return sweep ? launch_t<K, 1, true>(fa, fb, k, plus1, src, out, st)
+                 : launch_t<K, 1, false>(fa, fb, k, plus1, src, out, st);
+  }
+  return sweep ? launch_t<K, 2, true>(fa, fb, k, plus1, src, out, st)
+               : launch_t<K, 2, false>(fa, fb, k, plus1, src, out, st);
+}
+
+}  // namespace
+
+cudaError_t launch_ksg_sorted(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
+                              const PairOut& out, cudaStream_t st) {
+  switch (k) {
+    case 1: return launch_k<1>(fa, fb, k, plus1, src, out, st);
+    case 2: return launch_k<2>(fa, fb, k, plus1, src, out, st);
+    case 3: return launch_k<3>(fa, fb, k, plus1, src, out, st);
+    case 4: return launch_k<4>(fa, fb, k, plus1, src, out, st);
+    case 5: return launch_k<5>(fa, fb, k, plus1, src, out, st);
+    case 6: return launch_k<6>(fa, fb, k, plus1, src, out, st);
+    case 7: return launch_k<7>(fa, fb, k, plus1, src, out, st);
+    case 8: return launch_k<8>(fa, fb, k, plus1, src, out, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t ksg_comparisons(unsigned long long* value, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(value, g_ksg_comparisons, sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long zero = 0;
+    e = cudaMemcpyToSymbol(g_ksg_comparisons, &zero, sizeof(zero));
+  }
+  return e;
+}
+
+}  // namespace corr
