@@ -239,18 +239,25 @@ def main():
     create_s = time.perf_counter() - t
 
     stream = torch.cuda.current_stream()
-    kev = []
+    ev = {"ksg": [], "pearson_sampled": [], "pearson_block": []}
+
+    def _ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
 
     def step(f, timed=False):
-        if timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+        t0 = _ev() if timed else None
         km, ka = cb.corr_region_max(f, None, cb.CORR_KSG, K_NN, Ash, Bsh, S, SEED)
-        if timed:
-            e1.record(stream)
-            kev.append((e0, e1))
+        t1 = _ev() if timed else None
         pm, pa = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, Ash, Bsh, S, SEED)
+        t2 = _ev() if timed else None
         fm, fa = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, myslab, fBb, 0, 0)
+        if timed:
+            t3 = _ev()
+            ev["ksg"].append((t0, t1))
+            ev["pearson_sampled"].append((t1, t2))
+            ev["pearson_block"].append((t2, t3))
         if world > 1:
             km, ka = cdist.gather_region_results(km, ka, bounds)
             pm, pa = cdist.gather_region_results(pm, pa, bounds)
@@ -272,6 +279,7 @@ def main():
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()
+    cb.corr_ksg_comparisons(local, reset=True)
     l0 = cb.launch_count()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -280,22 +288,27 @@ def main():
     t1.record(stream)
     torch.cuda.synchronize()
     launches = cb.launch_count() - l0
+    executed = cb.corr_ksg_comparisons(local, reset=True) / args.steps
     if world > 1:
         tdist.barrier()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
-    ksg_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    stage_ms = {k: float(np.mean([a.elapsed_time(b) for a, b in v])) for k, v in ev.items()}
     if world > 1:
-        tt = torch.tensor([ms, ksg_ms], dtype=torch.float64, device=f"cuda:{local}")
+        tt = torch.tensor([ms] + [stage_ms[k] for k in ev], dtype=torch.float64, device=f"cuda:{local}")
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        ms, ksg_ms = float(tt[0]), float(tt[1])
+        ms = float(tt[0])
+        stage_ms = {k: float(tt[i + 1]) for i, k in enumerate(ev)}
     total_pairs = R * S
     value = total_pairs / (ms / 1e3)
 
-    # roofline of the dominant kernel (KSG k-NN, ALU-bound): algorithmic member-comparisons
+    # roofline of the dominant kernel (KSG, ALU-bound).  The exact sweep skips comparisons that
+    # cannot change any eps_i, so the per-unit figure is the EXECUTED member-comparisons
+    # ("report pairs/s and executed comparisons, never dense-equivalent").
     n = spec.members
     my_pairs = (hi - lo) * S
-    achieved = my_pairs * n * (n - 1) / (ksg_ms / 1e3)
+    ksg_ms = stage_ms["ksg"]
+    achieved = executed / (ksg_ms / 1e3)
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
     sm_max = peaks.get("sm_max_mhz") or clk.get("sm_max_mhz") or 1965.0
     peak = 148 * 128 * sm_max * 1e6 / 4.0
@@ -303,15 +316,36 @@ def main():
     if os.path.exists(NCU_TRAFFIC):
         try:
             tr = json.load(open(NCU_TRAFFIC))
-            traffic = tr.get("ksg_bytes_per_pair", 0) * my_pairs or None
+            traffic = tr.get("ksg_dram_bytes_per_pair", 0) * my_pairs or None
         except Exception:
             traffic = None
-    roofline = {"bound": "alu", "kernel": "ksg_kernel<3,8> (k-NN + counts + psi)", "achieved": achieved / 1e9,
-                "peak": peak / 1e9, "unit": "Gcmp/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_basis": f"148 SMs x 128 fp32 lanes x {sm_max:.0f} MHz / 4 ops per comparison",
+    roofline = {"bound": "alu", "kernel": "ksg_sorted_kernel<3,1,sweep> (k-NN + counts + psi)",
+                "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcmp/s", "frac": achieved / peak,
+                "traffic": traffic,
+                "peak_basis": f"148 SMs x 128 fp32 lanes x {sm_max:.0f} MHz / 4 ops per member-comparison",
                 "frac_at_measured_clock": (achieved / (148 * 128 * clk["sm_mhz"] * 1e6 / 4.0)
                                            if clk.get("sm_mhz") else None),
-                "ksg_ms_per_step": ksg_ms}
+                "executed_comparisons_per_pair": executed / max(my_pairs, 1),
+                "dense_comparisons_per_pair": n * (n - 1),
+                "ksg_ms_per_step": ksg_ms, "algorithmic_bytes_per_pair": 14 * spec.members}
+    # secondary: the focus-block GEMM (tensor-bound) and the sampled Pearson pairs (HBM/L2-bound)
+    fa_box, fb_box = slabs[rank], fB
+    nA = (fa_box[3] - fa_box[0]) * (fa_box[4] - fa_box[1]) * (fa_box[5] - fa_box[2])
+    nB = (fb_box[3] - fb_box[0]) * (fb_box[4] - fb_box[1]) * (fb_box[5] - fb_box[2])
+    tf32_peak = (peaks.get("bf16_tflops") or 1664.4) * 0.5
+    blk_tflops = 3 * 2.0 * nA * nB * n / (stage_ms["pearson_block"] / 1e3) / 1e12
+    roofline_block = {"bound": "tensor", "kernel": "pearson_block_kernel (tcgen05 kind::tf32, 3 MMAs/k-step)",
+                      "achieved": blk_tflops, "peak": tf32_peak, "unit": "TFLOP/s", "frac": blk_tflops / tf32_peak,
+                      "peak_basis": "measured bf16 dense x 0.5 (nominal tf32:bf16 ratio)",
+                      "pairs_per_s": nA * nB / (stage_ms["pearson_block"] / 1e3),
+                      "ms_per_step": stage_ms["pearson_block"]}
+    ps_gbs = my_pairs * (8 * spec.n_pad if hasattr(spec, "n_pad") else 8 * ((n + 7) // 8 * 8)) / (
+        stage_ms["pearson_sampled"] / 1e3) / 1e9
+    roofline_pearson_pairs = {"bound": "hbm", "kernel": "pearson_pairs_kernel", "achieved": ps_gbs,
+                              "peak": peaks.get("hbm_gbs") or 6552.3, "unit": "GB/s",
+                              "frac": ps_gbs / (peaks.get("hbm_gbs") or 6552.3),
+                              "pairs_per_s": my_pairs / (stage_ms["pearson_sampled"] / 1e3),
+                              "ms_per_step": stage_ms["pearson_sampled"]}
 
     # e2e: same metric from HOST memory through the C ABI (field upload + ingest per step)
     e2e = None
@@ -365,7 +399,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, args, world),
-                "roofline": roofline, "cpu_baseline": cpu_base, "e2e": e2e, "clocks": clk,
+                "roofline": roofline, "roofline_pearson_block": roofline_block,
+                "roofline_pearson_pairs": roofline_pearson_pairs, "cpu_baseline": cpu_base, "e2e": e2e, "clocks": clk,
                 "gpu_launches": launches, "field_create_s": create_s,
                 "region_max_sample": [float(res[0][0]), int(res[1][0][0]), int(res[1][0][1])]}
         print(json.dumps(line), flush=True)

@@ -61,24 +61,28 @@ __device__ __forceinline__ void merge2(float (&l)[K], float d0, float d1) {
   for (int r = 0; r < K; ++r) l[r] = nl[r];
 }
 
-// strict marginal count on a sorted array with element stride `st`:
-//   u = first s >= v with fl(s - v) >= e;  w = first s with s >= v or fl(v - s) < e
-//   count = (u - w) - [e > 0]        (the member itself lies in [w, u) iff e > 0)
-__device__ __forceinline__ int marginal_count(const float* __restrict__ S, int st, int n, float v, float e) {
-  int lo = 0, len = n;
-  while (len > 0) {
+// Strict marginal count of a member with value v and radius e on a sorted
+// array S (element stride ST): #{j != i : |fl(v - S_j)| < e}.
+//   e == 0: the strict interval is empty -> 0 (reading R5).
+//   e  > 0: u = first s with fl(s - v) >= e, w = first s with fl(v - s) < e (both predicates
+//           are monotone in s by monotone rounding, and imply / cover s >= v because e > 0);
+//           [w, u) holds every s with |fl(s - v)| < e, the member itself included -> u - w - 1.
+// Branch-free lower bounds (uniform trip count), the two searches interleaved for ILP.
+template <int ST>
+__device__ __forceinline__ int marginal_count(const float* __restrict__ S, int n, float v, float e) {
+  if (!(e > 0.f)) return 0;
+  int bu = 0, bw = 0, len = n;
+  while (len > 1) {
     const int half = len >> 1;
-    const float s = S[(lo + half) * st];
-    if ((s >= v) && (s - v >= e)) len = half; else { lo += half + 1; len -= half + 1; }
+    const float su = S[(bu + half - 1) * ST];
+    const float sw = S[(bw + half - 1) * ST];
+    bu = (su - v >= e) ? bu : bu + half;   // not yet P_u -> move right
+    bw = (v - sw < e) ? bw : bw + half;    // not yet P_w -> move right
+    len -= half;
   }
-  const int u = lo;
-  lo = 0; len = n;
-  while (len > 0) {
-    const int half = len >> 1;
-    const float s = S[(lo + half) * st];
-    if ((s >= v) || (v - s < e)) len = half; else { lo += half + 1; len -= half + 1; }
-  }
-  return (u - lo) - (e > 0.f ? 1 : 0);
+  const int u = bu + ((S[bu * ST] - v >= e) ? 0 : 1);
+  const int w = bw + ((v - S[bw * ST] < e) ? 0 : 1);
+  return u - w - 1;
 }
 
 // own-block chunk: exact network; the self pair j == i exists only for member RC of each lane
@@ -99,6 +103,23 @@ __device__ __forceinline__ void own_chunk(const float4* __restrict__ cp, const f
       merge2<K>(l[rr], e0, e1);
     }
   }
+}
+
+template <int K>
+__device__ __forceinline__ void insert1(float (&l)[K], float d) {
+#pragma unroll
+  for (int t = K - 1; t >= 1; --t) l[t] = fminf(l[t], fmaxf(l[t - 1], d));
+  l[0] = fminf(l[0], d);
+}
+
+// RM == 1 own chunk without masks: lane L reads the warp's 32 joint samples rotated by L
+// (a private doubled copy, dup[i] = chunk[i & 31]); s = 1..31 visits every j != i exactly once.
+template <int K>
+__device__ __forceinline__ void own_rotated(const float2* __restrict__ dup, int lane, float2 zi, float (&l)[K]) {
+  const float2* p = dup + lane;
+#pragma unroll
+  for (int s = 1; s < 31; s += 2) merge2<K>(l, cheb(zi, p[s]), cheb(zi, p[s + 1]));
+  insert1<K>(l, cheb(zi, p[31]));
 }
 
 template <int K, int RM, int RC>
@@ -170,6 +191,7 @@ __global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
   uint16_t* pm = reinterpret_cast<uint16_t*>(tb + n_pad);
   double* red = reinterpret_cast<double*>(pm + n_pad + 8);
   int* next_blk = reinterpret_cast<int*>(red + 32);
+  float2* dupbuf = reinterpret_cast<float2*>(red + 34);  // [8 warps][64] (RM == 1 own chunk)
 
   for (int i = threadIdx.x; i < n + 2; i += nthreads) psi[i] = psi_g[i];
   __syncthreads();
@@ -235,7 +257,17 @@ __global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
       }
       const int c0 = mb * RM;
       const int c1 = min(c0 + RM, nch);
-      OwnBlock<K, RM, RM - 1>::run(xy4, c0, nch, zi, l, lane);
+      if constexpr (RM == 1) {
+        float2* dup = dupbuf + warp * 64;
+        const float2 zc = xy[c0 * 32 + lane];
+        dup[lane] = zc;
+        dup[lane + 32] = zc;
+        __syncwarp();
+        own_rotated<K>(dup, lane, zi[0], l[0]);
+        __syncwarp();
+      } else {
+        OwnBlock<K, RM, RM - 1>::run(xy4, c0, nch, zi, l, lane);
+      }
       int nproc = c1 - c0;
       int clo = c0 - 1, chi = c1;
       const float xblk_lo = xy[mb * BLK].x;
@@ -273,8 +305,8 @@ __global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
       for (int rr = 0; rr < RM; ++rr) {
         if (ts[rr] < n) {
           const float e = l[rr][K - 1];
-          const int cu = marginal_count(reinterpret_cast<const float*>(xy), 2, n, zi[rr].x, e);
-          const int cv = marginal_count(sy, 1, n, zi[rr].y, e);
+          const int cu = marginal_count<2>(reinterpret_cast<const float*>(xy), n, zi[rr].x, e);
+          const int cv = marginal_count<1>(sy, n, zi[rr].y, e);
           acc += psi[cu + off] + psi[cv + off];
           if (out.dbg_eps) {
             const int m = pm[ts[rr]];
@@ -314,7 +346,7 @@ cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus
   const int nblk = (n + 32 * RM - 1) / (32 * RM);
   const size_t smem = (size_t)((n + 2 + 1) & ~1) * sizeof(double) + (size_t)nxy * sizeof(float2) +
                       2 * (size_t)n_pad * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
-                      32 * sizeof(double) + 16;
+                      34 * sizeof(double) + 8 * 64 * sizeof(float2);
   auto kern = ksg_sorted_kernel<K, RM, SWEEP>;
   const int warps = nblk < 8 ? nblk : 8;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
