@@ -68,20 +68,31 @@ __device__ __forceinline__ void merge2(float (&l)[K], float d0, float d1) {
 //           are monotone in s by monotone rounding, and imply / cover s >= v because e > 0);
 //           [w, u) holds every s with |fl(s - v)| < e, the member itself included -> u - w - 1.
 // Branch-free lower bounds (uniform trip count), the two searches interleaved for ILP.
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
 template <int ST>
 __device__ __forceinline__ int marginal_count(const float* __restrict__ S, int n, float v, float e) {
   if (!(e > 0.f)) return 0;
-  int bu = 0, bw = 0, len = n;
+  // 32-bit shared-memory byte addresses: one IADD + one SEL per probe and search
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(S);
+  uint32_t au = base, aw = base;
+  int len = n;
   while (len > 1) {
     const int half = len >> 1;
-    const float su = S[(bu + half - 1) * ST];
-    const float sw = S[(bw + half - 1) * ST];
-    bu = (su - v >= e) ? bu : bu + half;   // not yet P_u -> move right
-    bw = (v - sw < e) ? bw : bw + half;    // not yet P_w -> move right
+    const uint32_t step = (uint32_t)(half * ST * 4);
+    const float su = lds_f32(au + step - ST * 4);
+    const float sw = lds_f32(aw + step - ST * 4);
+    au = (su - v >= e) ? au : au + step;   // not yet P_u -> move right
+    aw = (v - sw < e) ? aw : aw + step;    // not yet P_w -> move right
     len -= half;
   }
-  const int u = bu + ((S[bu * ST] - v >= e) ? 0 : 1);
-  const int w = bw + ((v - S[bw * ST] < e) ? 0 : 1);
+  const int bu = (int)((au - base) / (ST * 4)), bw = (int)((aw - base) / (ST * 4));
+  const int u = bu + ((lds_f32(au) - v >= e) ? 0 : 1);
+  const int w = bw + ((v - lds_f32(aw) < e) ? 0 : 1);
   return u - w - 1;
 }
 
@@ -135,39 +146,44 @@ struct OwnBlock<K, RM, -1> {
   __device__ __forceinline__ static void run(const float4*, int, int, const float2 (&)[RM], float (&)[RM][K], int) {}
 };
 
-// one filtered 32-j chunk
-template <int K, int RM, bool DESC>
+// one filtered 32-j chunk, groups of G j's (G = 4 or 8) per vote
+template <int K, int RM, int G, bool DESC>
 __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
                                                float (&l)[RM][K]) {
+  constexpr int NG = 32 / G;
 #pragma unroll 2
-  for (int gi = 0; gi < 8; ++gi) {
-    const int g = DESC ? 7 - gi : gi;
-    const float4 v0 = cp[2 * g], v1 = cp[2 * g + 1];
-    const float2 z0 = make_float2(v0.x, v0.y), z1 = make_float2(v0.z, v0.w);
-    const float2 z2 = make_float2(v1.x, v1.y), z3 = make_float2(v1.z, v1.w);
-    float d[RM][4];
+  for (int gi = 0; gi < NG; ++gi) {
+    const int g = DESC ? NG - 1 - gi : gi;
+    float2 z[G];
+#pragma unroll
+    for (int q = 0; q < G / 2; ++q) {
+      const float4 v = cp[g * (G / 2) + q];
+      z[2 * q] = make_float2(v.x, v.y);
+      z[2 * q + 1] = make_float2(v.z, v.w);
+    }
+    float d[RM][G];
     bool p = false;
 #pragma unroll
     for (int rr = 0; rr < RM; ++rr) {
-      d[rr][0] = cheb(zi[rr], z0);
-      d[rr][1] = cheb(zi[rr], z1);
-      d[rr][2] = cheb(zi[rr], z2);
-      d[rr][3] = cheb(zi[rr], z3);
-      const float m = fminf(fminf(fminf(d[rr][0], d[rr][1]), d[rr][2]), d[rr][3]);
+#pragma unroll
+      for (int q = 0; q < G; ++q) d[rr][q] = cheb(zi[rr], z[q]);
+      float m = d[rr][0];
+#pragma unroll
+      for (int q = 1; q < G; ++q) m = fminf(m, d[rr][q]);
       p |= m < l[rr][K - 1];
     }
     if (__any_sync(0xffffffffu, p)) {
 #pragma unroll
       for (int rr = 0; rr < RM; ++rr) {
-        merge2<K>(l[rr], d[rr][0], d[rr][1]);
-        merge2<K>(l[rr], d[rr][2], d[rr][3]);
+#pragma unroll
+        for (int q = 0; q < G; q += 2) merge2<K>(l[rr], d[rr][q], d[rr][q + 1]);
       }
     }
   }
 }
 
-template <int K, int RM, bool SWEEP>
-__global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
+template <int K, int RM, int G, bool SWEEP>
+__global__ void __launch_bounds__(256, (RM == 1 ? 4 : 3)) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
     const float* __restrict__ Sb, const uint16_t* __restrict__ Pb, const float* __restrict__ Fb,
     const float* __restrict__ spa, const float* __restrict__ spb, const uint8_t* __restrict__ ca,
@@ -284,7 +300,7 @@ __global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
           if (SWEEP && (xblk_lo - xy[clo * 32 + 31].x) >= tmax) {
             clo = -1;
           } else {
-            chunk_filtered<K, RM, true>(xy4 + clo * 16, zi, l);
+            chunk_filtered<K, RM, G, true>(xy4 + clo * 16, zi, l);
             --clo;
             ++nproc;
           }
@@ -293,7 +309,7 @@ __global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
           if (SWEEP && (xy[chi * 32].x - xblk_hi) >= tmax) {
             chi = nch;
           } else {
-            chunk_filtered<K, RM, false>(xy4 + chi * 16, zi, l);
+            chunk_filtered<K, RM, G, false>(xy4 + chi * 16, zi, l);
             ++chi;
             ++nproc;
           }
@@ -338,7 +354,7 @@ __global__ void __launch_bounds__(256, 3) ksg_sorted_kernel(
   if (lane == 0 && executed) atomicAdd(&g_ksg_comparisons, executed);
 }
 
-template <int K, int RM, bool SWEEP>
+template <int K, int RM, int G, bool SWEEP>
 cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                      const PairOut& out, cudaStream_t st) {
   const int n = fa->n, n_pad = fa->n_pad;
@@ -347,7 +363,7 @@ cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus
   const size_t smem = (size_t)((n + 2 + 1) & ~1) * sizeof(double) + (size_t)nxy * sizeof(float2) +
                       2 * (size_t)n_pad * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
                       34 * sizeof(double) + 8 * 64 * sizeof(float2);
-  auto kern = ksg_sorted_kernel<K, RM, SWEEP>;
+  auto kern = ksg_sorted_kernel<K, RM, G, SWEEP>;
   const int warps = nblk < 8 ? nblk : 8;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -373,19 +389,20 @@ template <int K>
 cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                      const PairOut& out, cudaStream_t st) {
   // CORR_KSG_SWEEP=0 disables the exact sweep (dense n(n-1) comparisons); CORR_KSG_RM picks
-  // members per lane (1, 2 or 4).
+  // members per lane (1, 2 or 4) and CORR_KSG_G the filter group (4, or 8 with RM = 1).
   static const int sweep = env_int("CORR_KSG_SWEEP", 1);
-  static const int rm = env_int("CORR_KSG_RM", 2);
-  if (rm == 4) {
-    return sweep ? launch_t<K, 4, true>(fa, fb, k, plus1, src, out, st)
-                 : launch_t<K, 4, false>(fa, fb, k, plus1, src, out, st);
-  }
-  if (rm == 1) {
-    return sweep ? launch_t<K, 1, true>(fa, fb, k, plus1, src, out, st)
-                 : launch_t<K, 1, false>(fa, fb, k, plus1, src, out, st);
-  }
-  return sweep ? launch_t<K, 2, true>(fa, fb, k, plus1, src, out, st)
-               : launch_t<K, 2, false>(fa, fb, k, plus1, src, out, st);
+  static const int rm = env_int("CORR_KSG_RM", 1);
+  static const int g = env_int("CORR_KSG_G", 4);
+#define CORR_KSG_CASE(RMv, Gv)                                                 \
+  if (rm == RMv && g == Gv)                                                   \
+    return sweep ? launch_t<K, RMv, Gv, true>(fa, fb, k, plus1, src, out, st) \
+                 : launch_t<K, RMv, Gv, false>(fa, fb, k, plus1, src, out, st);
+  CORR_KSG_CASE(1, 8)
+  CORR_KSG_CASE(2, 4)
+  CORR_KSG_CASE(4, 4)
+#undef CORR_KSG_CASE
+  return sweep ? launch_t<K, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+               : launch_t<K, 1, 4, false>(fa, fb, k, plus1, src, out, st);
 }
 
 }  // namespace
