@@ -255,7 +255,7 @@ static int eval_pairs_impl(const corr_field* fa, const corr_field* fb, int32_t m
   cudaError_t e;
   if ((measure & 0xFF) == CORR_KSG) {
     e = launch_ksg(fa, fb, k, (measure & CORR_F_KSG_PLUS1) != 0, src, po, st);
-    if (e == cudaErrorNotSupported) return fail(CORR_E_INVAL, "KSG with k > 8 is not implemented yet");
+    if (e == cudaErrorNotSupported) return fail(CORR_E_INVAL, "KSG with k > 32 is not supported");
   } else {
     e = launch_pearson_pairs(fa, fb, src, po, st);
   }
@@ -350,7 +350,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
       if (e == cudaErrorNotSupported) {
         cudaFreeAsync(dreg, st);
         cudaFreeAsync(keys, st);
-        return fail(CORR_E_INVAL, "KSG with k > 8 is not implemented yet");
+        return fail(CORR_E_INVAL, "KSG with k > 32 is not supported");
       }
     } else if (samples == 0) {
       e = launch_pearson_block(fa, fb, reg.data(), dreg, nregion_pairs, po.absval, keys, st);

@@ -235,7 +235,11 @@ __global__ void __launch_bounds__(256) ksg_kernel(const float* __restrict__ Fa, 
 template <int K>
 cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                      const PairOut& out, cudaStream_t st) {
-  if (fa->n > kBlockMembers) return launch_ksg_sorted(fa, fb, k, plus1, src, out, st);
+  static const int small_sorted = [] {
+    const char* s = getenv("CORR_KSG_SMALL");  // "warp" keeps the one-warp-per-pair kernel
+    return (s && s[0] == 'w') ? 0 : 1;
+  }();
+  if (fa->n > kBlockMembers || small_sorted || k > 8) return launch_ksg_sorted(fa, fb, k, plus1, src, out, st);
   const int n = fa->n, n_pad = fa->n_pad;
   const int nblk = (n + kBlockMembers - 1) / kBlockMembers;
   const int nxy = nblk * kBlockMembers;
@@ -282,6 +286,7 @@ cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus
 cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                        const PairOut& out, cudaStream_t st) {
   if (src.nunits == 0) return cudaSuccess;
+  if (k > 8) return launch_ksg_sorted(fa, fb, k, plus1, src, out, st);
   switch (k) {
     case 1: return launch_k<1>(fa, fb, k, plus1, src, out, st);
     case 2: return launch_k<2>(fa, fb, k, plus1, src, out, st);

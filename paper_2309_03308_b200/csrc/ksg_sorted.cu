@@ -183,7 +183,7 @@ __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, co
 }
 
 template <int K, int RM, int G, bool SWEEP>
-__global__ void __launch_bounds__(256, (RM == 1 ? 4 : 3)) ksg_sorted_kernel(
+__global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
     const float* __restrict__ Sb, const uint16_t* __restrict__ Pb, const float* __restrict__ Fb,
     const float* __restrict__ spa, const float* __restrict__ spb, const uint8_t* __restrict__ ca,
@@ -320,7 +320,12 @@ __global__ void __launch_bounds__(256, (RM == 1 ? 4 : 3)) ksg_sorted_kernel(
 #pragma unroll
       for (int rr = 0; rr < RM; ++rr) {
         if (ts[rr] < n) {
-          const float e = l[rr][K - 1];
+          float e = l[rr][K - 1];
+          if (K > 8) {  // list longer than k: eps = l[k-1] (the K smallest are exact)
+#pragma unroll
+            for (int t = 0; t < K - 1; ++t)
+              if (t == k - 1) e = l[rr][t];
+          }
           const int cu = marginal_count<2>(reinterpret_cast<const float*>(xy), n, zi[rr].x, e);
           const int cv = marginal_count<1>(sy, n, zi[rr].y, e);
           acc += psi[cu + off] + psi[cv + off];
@@ -418,8 +423,21 @@ cudaError_t launch_ksg_sorted(const corr_field* fa, const corr_field* fb, int k,
     case 6: return launch_k<6>(fa, fb, k, plus1, src, out, st);
     case 7: return launch_k<7>(fa, fb, k, plus1, src, out, st);
     case 8: return launch_k<8>(fa, fb, k, plus1, src, out, st);
-    default: return cudaErrorNotSupported;
+    default: break;
   }
+  // NEXT #2 (paper default k = ceil(3n/100)): register lists of 12/16/24/32;
+  // inserting d >= l[KT-1] >= l[k-1] cannot change the k smallest, so the filter and the sweep
+  // stay exact with the longer list, and eps = l[k-1].
+  const bool sweep = env_int("CORR_KSG_SWEEP", 1) != 0;
+  if (k <= 12) return sweep ? launch_t<12, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<12, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  if (k <= 16) return sweep ? launch_t<16, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<16, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  if (k <= 24) return sweep ? launch_t<24, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<24, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  if (k <= 32) return sweep ? launch_t<32, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<32, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  return cudaErrorNotSupported;
 }
 
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset) {

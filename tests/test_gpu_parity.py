@@ -78,13 +78,22 @@ def test_c1_eps_counts_bit_exact():
 
 @pytest.mark.parametrize("n,k,dims", [(100, 3, (16, 16, 4)), (1000, 3, (8, 8, 4)), (37, 1, (8, 8, 2)),
                                       (130, 5, (8, 8, 2)), (257, 8, (8, 4, 2)), (1001, 4, (4, 4, 2)),
-                                      (4, 3, (8, 8, 1)), (129, 2, (8, 4, 2))])
+                                      (4, 3, (8, 8, 1)), (129, 2, (8, 4, 2)), (1000, 30, (4, 4, 2)),
+                                      (200, 12, (8, 4, 2)), (300, 17, (8, 4, 2)), (1000, 0, (4, 4, 2)),
+                                      (64, 32, (8, 4, 2))])
 def test_eps_counts_mi_bit_exact_ragged(n, k, dims):
+    """k = 0 selects the paper's ceil(3n/100); k > 8 uses the long-list kernels."""
     spec = synth.field_spec(*dims, n, seed=100 + n)
     vals, f = _field(spec)
     a, b = synth.random_pairs(spec.points, 300 if n <= 300 else 60, seed=n)
     a, b = a.numpy(), b.numpy()
-    _check_knn(f, vals, k, a, b)
+    kk = k if k else min(max(1, -(-3 * n // 100)), n - 1)
+    _check_knn(f, vals, kk, a, b)
+    if k == 0:
+        e0, _, _ = cb.corr_ksg_debug(f, None, 0, torch.from_numpy(a[:4]).cuda(), torch.from_numpy(b[:4]).cuda())
+        e1, _, _ = cb.corr_ksg_debug(f, None, kk, torch.from_numpy(a[:4]).cuda(), torch.from_numpy(b[:4]).cuda())
+        assert torch.equal(e0, e1)
+    k = kk
     got = _cpu(cb.corr_eval_pairs(f, None, cb.CORR_KSG, k, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()))
     ref = oracle.eval_pairs(vals.cpu(), None, oracle.KSG, k, a, b)
     assert np.array_equal(np.isnan(got), np.isnan(ref))
