@@ -62,6 +62,18 @@ enum { CORR_OK = 0, CORR_E_INVAL = -1, CORR_E_RANGE = -2, CORR_E_NOMEM = -3, COR
 int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, int32_t members,
                       int32_t device, void* cuda_stream, corr_field** out);
 
+/* corr_field_aggregate -- one level of the paper's mean-tree (§3.3: "for each
+ * brick and each ensemble member ... the means ... of all variables at the grid points represented
+ * by this brick"): a new field on the grid ceil(nx/fx) x ceil(ny/fy) x ceil(nz/fz) whose series at
+ * coarse point (X,Y,Z) is, per member, the mean of the fine series over the block
+ * [fx*X, fx*X+fx) x [fy*Y, ...) x [fz*Z, ...) (boundary blocks average the points that exist;
+ * fp64 sums, fp32 result).  Same members and device as `f`; all derived buffers are rebuilt, so
+ * every call above works on the aggregate ("BOS ... using the mean values at the highest
+ * resolution tree-level that just fits into GPU memory").  Synchronises the stream.
+ * Errors: CORR_E_INVAL (factor < 1), CORR_E_NOMEM, CORR_E_CUDA.  Release with corr_field_destroy. */
+int corr_field_aggregate(const corr_field* f, int32_t fx, int32_t fy, int32_t fz, void* cuda_stream,
+                         corr_field** out);
+
 /* Frees the field's device memory (device-synchronising).  NULL is a no-op. */
 int corr_field_destroy(corr_field* f);
 

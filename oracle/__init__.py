@@ -170,6 +170,22 @@ def sample(seed: int, A, B, s: int, nx: int, ny: int) -> Tuple[int, int]:
     return pa.value, pb.value
 
 
+def aggregate_mean(values, dims, fx: int, fy: int, fz: int) -> np.ndarray:
+    """Mean-tree level (§3.3): per member, the mean of the series over each
+    fx x fy x fz block of grid points (boundary blocks average the points that exist),
+    summed in fp64 and rounded to fp32.  values: [n, P] in file order; returns [n, P']."""
+    nx, ny, nz = dims
+    v = _field(values).reshape(-1, nz, ny, nx).astype(np.float64)
+    cx, cy, cz = -(-nx // fx), -(-ny // fy), -(-nz // fz)
+    out = np.empty((v.shape[0], cz, cy, cx), np.float64)
+    for Z in range(cz):
+        for Y in range(cy):
+            for X in range(cx):
+                blk = v[:, Z * fz:(Z + 1) * fz, Y * fy:(Y + 1) * fy, X * fx:(X + 1) * fx]
+                out[:, Z, Y, X] = blk.reshape(blk.shape[0], -1).sum(axis=1) / blk[0].size
+    return out.reshape(v.shape[0], -1).astype(np.float32)
+
+
 def _box_points(box, nx, ny):
     x0, y0, z0, x1, y1, z1 = box
     z, y, x = np.meshgrid(np.arange(z0, z1), np.arange(y0, y1), np.arange(x0, x1), indexing="ij")

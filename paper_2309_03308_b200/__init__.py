@@ -6,5 +6,5 @@ package holds its thin binding (``binding``), the seeded input generator (``synt
 and the multi-GPU sharding helpers (``dist``).
 """
 from .binding import (CORR_F_ABS, CORR_F_KSG_PLUS1, CORR_KSG, CORR_PEARSON, CorrError, Field,  # noqa: F401
-                      corr_check, corr_eval_pairs, corr_field_create, corr_field_destroy, corr_field_info,
+                      corr_check, corr_eval_pairs, corr_field_aggregate, corr_field_create, corr_field_destroy, corr_field_info,
                       corr_ksg_debug, corr_region_max)

@@ -22,7 +22,7 @@ CORR_F_KSG_PLUS1 = 1 << 8
 CORR_F_ABS = 1 << 9
 CORR_OK, CORR_E_INVAL, CORR_E_RANGE, CORR_E_NOMEM, CORR_E_CUDA = 0, -1, -2, -3, -4
 
-EXPORTS = ("corr_field_create", "corr_field_destroy", "corr_field_info", "corr_eval_pairs",
+EXPORTS = ("corr_field_create", "corr_field_aggregate", "corr_field_destroy", "corr_field_info", "corr_eval_pairs",
            "corr_region_max", "corr_ksg_debug", "corr_check", "corr_ksg_comparisons", "corr_launch_count",
            "corr_last_error")
 
@@ -55,6 +55,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
     L.corr_field_create.argtypes = [vp, i32, i32, i32, i32, i32, vp, ctypes.POINTER(vp)]
     L.corr_field_destroy.argtypes = [vp]
+    L.corr_field_aggregate.argtypes = [vp, i32, i32, i32, vp, ctypes.POINTER(vp)]
     L.corr_field_info.argtypes = [vp] + [ctypes.POINTER(i32)] * 5
     L.corr_eval_pairs.argtypes = [vp, vp, i32, i32, vp, vp, i64, vp, vp]
     L.corr_region_max.argtypes = [vp, vp, i32, i32, ctypes.POINTER(corr_box), ctypes.POINTER(corr_box), i64,
@@ -131,6 +132,16 @@ def corr_field_create(values, nx: int, ny: int, nz: int, members: int, device: O
     _check(L.corr_field_create(ctypes.c_void_p(_ptr(values)), nx, ny, nz, members, device,
                                ctypes.c_void_p(st), ctypes.byref(h)))
     return Field(h.value, nx, ny, nz, members, device)
+
+
+def corr_field_aggregate(field: Field, fx: int, fy: int, fz: int, stream=None) -> Field:
+    """Mean-tree level of `field`: block means of fx x fy x fz points."""
+    h = ctypes.c_void_p()
+    with torch.cuda.device(field.device):
+        st = _stream(stream)
+    _check(load().corr_field_aggregate(ctypes.c_void_p(field.handle), fx, fy, fz, ctypes.c_void_p(st),
+                                       ctypes.byref(h)))
+    return Field(h.value, -(-field.nx // fx), -(-field.ny // fy), -(-field.nz // fz), field.members, field.device)
 
 
 def corr_field_destroy(field: Field):

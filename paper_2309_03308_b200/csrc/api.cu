@@ -77,6 +77,44 @@ std::vector<double> digamma_table(int n) {
   return t;
 }
 
+// Allocates every device buffer of a field and uploads its psi table (stream-ordered).
+int alloc_field(int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t device, cudaStream_t st,
+                corr_field** out) {
+  corr_field* f = new corr_field();
+  memset(f, 0, sizeof(*f));
+  f->device = device;
+  f->nx = nx; f->ny = ny; f->nz = nz;
+  f->n = members;
+  f->n_pad = (members + 7) / 8 * 8;
+  f->P = (int64_t)nx * ny * nz;
+  const size_t row_elems = (size_t)f->P * f->n_pad;
+  auto alloc = [&](void** p, size_t bytes) -> bool {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  };
+  if (!alloc((void**)&f->F, row_elems * 4) || !alloc((void**)&f->Z, row_elems * 4) ||
+      !alloc((void**)&f->Zhi, row_elems * 4) || !alloc((void**)&f->Zlo, row_elems * 4) ||
+      !alloc((void**)&f->S, row_elems * 4) || !alloc((void**)&f->perm, row_elems * 2) ||
+      !alloc((void**)&f->cflag, (size_t)f->P) || !alloc((void**)&f->spread, (size_t)f->P * 4) ||
+      !alloc((void**)&f->psi, ((size_t)members + 2) * 8) || !alloc((void**)&f->err, sizeof(int))) {
+    free_field(f);
+    return fail(CORR_E_NOMEM, "device allocation failed for the field");
+  }
+  const std::vector<double> psi = digamma_table(members);
+  cudaError_t e = cudaMemcpyAsync(f->psi, psi.data(), psi.size() * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(f->err, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // psi is a stack vector
+  if (e != cudaSuccess) {
+    free_field(f);
+    return cuda_fail(e, "field allocation");
+  }
+  *out = f;
+  return CORR_OK;
+}
+
 int check_pair_fields(const corr_field* fa, const corr_field*& fb) {
   if (!fa) return fail(CORR_E_INVAL, "field is NULL");
   if (!fb) fb = fa;
@@ -133,22 +171,17 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
   if (members < 2) return fail(CORR_E_INVAL, "members must be >= 2 (SPEC.md:34)");
   if (members > 8192) return fail(CORR_E_INVAL, "members > 8192 not supported");
   int ndev = 0;
-  cudaError_t e = cudaGetDeviceCount(&ndev);
-  if (e != cudaSuccess || ndev == 0) return cuda_fail(e == cudaSuccess ? cudaErrorNoDevice : e, "corr_field_create");
+  const cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0) return cuda_fail(ce == cudaSuccess ? cudaErrorNoDevice : ce, "corr_field_create");
   if (device < 0 || device >= ndev) return fail(CORR_E_INVAL, "device ordinal out of range");
   DeviceGuard guard(device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   cudaStream_t st = (cudaStream_t)cuda_stream;
 
-  corr_field* f = new corr_field();
-  memset(f, 0, sizeof(*f));
-  f->device = device;
-  f->nx = nx; f->ny = ny; f->nz = nz;
-  f->n = members;
-  f->n_pad = (members + 7) / 8 * 8;
-  f->P = (int64_t)nx * ny * nz;
-  const size_t row_elems = (size_t)f->P * f->n_pad;
-
+  corr_field* f = nullptr;
+  const int arc = alloc_field(nx, ny, nz, members, device, st, &f);
+  if (arc) return arc;
+  cudaError_t e = cudaSuccess;
   auto alloc = [&](void** p, size_t bytes) -> bool {
     if (cudaMalloc(p, bytes) != cudaSuccess) {
       cudaGetLastError();
@@ -156,17 +189,6 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
     }
     return true;
   };
-  if (!alloc((void**)&f->F, row_elems * 4) || !alloc((void**)&f->Z, row_elems * 4) ||
-      !alloc((void**)&f->Zhi, row_elems * 4) || !alloc((void**)&f->Zlo, row_elems * 4) ||
-      !alloc((void**)&f->S, row_elems * 4) || !alloc((void**)&f->perm, row_elems * 2) ||
-      !alloc((void**)&f->cflag, (size_t)f->P) || !alloc((void**)&f->spread, (size_t)f->P * 4) || !alloc((void**)&f->psi, ((size_t)members + 2) * 8) ||
-      !alloc((void**)&f->err, sizeof(int))) {
-    free_field(f);
-    return fail(CORR_E_NOMEM, "device allocation failed for the field");
-  }
-  const std::vector<double> psi = digamma_table(members);
-  e = cudaMemcpyAsync(f->psi, psi.data(), psi.size() * 8, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(f->err, 0, sizeof(int), st);
 
   // values: device pointer on `device` -> used in place; otherwise staged through HBM
   const float* dvalues = values;
@@ -201,6 +223,29 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
     return fail(CORR_E_INVAL, "non-finite input value (SPEC.md:72)");
   }
   *out = f;
+  return CORR_OK;
+}
+
+int corr_field_aggregate(const corr_field* f, int32_t fx, int32_t fy, int32_t fz, void* cuda_stream,
+                         corr_field** out) {
+  if (!out) return fail(CORR_E_INVAL, "out is NULL");
+  *out = nullptr;
+  if (!f) return fail(CORR_E_INVAL, "field is NULL");
+  if (fx < 1 || fy < 1 || fz < 1) return fail(CORR_E_INVAL, "aggregation factors must be >= 1");
+  DeviceGuard guard(f->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  corr_field* g = nullptr;
+  const int rc = alloc_field((f->nx + fx - 1) / fx, (f->ny + fy - 1) / fy, (f->nz + fz - 1) / fz, f->n, f->device, st,
+                             &g);
+  if (rc) return rc;
+  cudaError_t e = launch_field_aggregate(f, g, fx, fy, fz, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    free_field(g);
+    return cuda_fail(e, "corr_field_aggregate");
+  }
+  *out = g;
   return CORR_OK;
 }
 

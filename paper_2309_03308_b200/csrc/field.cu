@@ -149,13 +149,53 @@ __global__ void __launch_bounds__(512) sort_kernel(const float* __restrict__ F, 
   }
 }
 
+// ---- 4. mean-tree level (§3.3): per-member block means ----------
+// One warp per coarse point; lanes stride over members, so every fine row is read with
+// coalesced loads and the coarse row is written contiguously.  fp64 sums, fp32 means; a
+// boundary block averages the fine points that exist (SPEC.md:59 voxel-count weighting).
+__global__ void __launch_bounds__(256) aggregate_kernel(const float* __restrict__ F, float* __restrict__ G,
+                                                        int nx, int ny, int nz, int cx, int cy, int cz, int fx,
+                                                        int fy, int fz, int n, int n_pad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (q >= (int64_t)cx * cy * cz) return;
+  const int X = (int)(q % cx), Y = (int)((q / cx) % cy), Z = (int)(q / ((int64_t)cx * cy));
+  const int x0 = X * fx, y0 = Y * fy, z0 = Z * fz;
+  const int x1 = min(nx, x0 + fx), y1 = min(ny, y0 + fy), z1 = min(nz, z0 + fz);
+  const double cnt = (double)((x1 - x0) * (y1 - y0) * (z1 - z0));
+  for (int e = lane; e < n_pad; e += 32) {
+    float out = 0.f;
+    if (e < n) {
+      double s = 0.0;
+      for (int z = z0; z < z1; ++z)
+        for (int y = y0; y < y1; ++y)
+          for (int x = x0; x < x1; ++x) s += (double)F[(((int64_t)z * ny + y) * nx + x) * n_pad + e];
+      out = (float)(s / cnt);
+    }
+    G[q * n_pad + e] = out;
+  }
+}
+
 }  // namespace
 
+cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int fx, int fy, int fz, cudaStream_t st) {
+  const int64_t threads = dst->P * 32;
+  aggregate_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(src->F, dst->F, src->nx, src->ny, src->nz,
+                                                                     dst->nx, dst->ny, dst->nz, fx, fy, fz, src->n,
+                                                                     src->n_pad);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_field_ingest(dst, nullptr, st);
+}
+
+// din == nullptr: F is already filled (aggregate levels); else transpose din [n][P] into F.
 cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st) {
   const int64_t P = f->P;
-  {
+  if (din) {
     dim3 grid((unsigned)((P + 31) / 32), (unsigned)((f->n_pad + 31) / 32));
     transpose_kernel<<<grid, 256, 0, st>>>(din, f->F, f->n, f->n_pad, P, f->err);
+    note_launch();
   }
   {
     const int64_t threads = P * 32;
@@ -178,7 +218,7 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
     const int64_t blocks = (P + rows_per_block - 1) / rows_per_block;
     sort_kernel<<<(unsigned)blocks, threads, smem, st>>>(f->F, f->S, f->perm, f->n, f->n_pad, P, log2n2);
   }
-  note_launch(3);
+  note_launch(2);
   return cudaGetLastError();
 }
 
