@@ -328,6 +328,22 @@ def main():
                 "executed_comparisons_per_pair": executed / max(my_pairs, 1),
                 "dense_comparisons_per_pair": n * (n - 1),
                 "ksg_ms_per_step": ksg_ms, "algorithmic_bytes_per_pair": 14 * spec.members}
+    # the same kernel with the sweep disabled (CORR_F_KSG_DENSE): all n(n-1) comparisons executed,
+    # results bit-identical -- the ALU-efficiency reference for the dense k-NN pass
+    Sd = 256
+    cb.corr_ksg_comparisons(local, reset=True)
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    cb.corr_region_max(field, None, cb.CORR_KSG | cb.CORR_F_KSG_DENSE, K_NN, Ash, Bsh, Sd, SEED)
+    d1.record(stream)
+    torch.cuda.synchronize()
+    dense_s = d0.elapsed_time(d1) / 1e3
+    dense_exec = cb.corr_ksg_comparisons(local, reset=True)
+    roofline_dense = {"bound": "alu", "kernel": "ksg_sorted_kernel<3,1,dense> (CORR_F_KSG_DENSE)",
+                      "achieved": (hi - lo) * Sd * n * (n - 1) / dense_s / 1e9, "peak": peak / 1e9, "unit": "Gcmp/s",
+                      "frac": (hi - lo) * Sd * n * (n - 1) / dense_s / peak,
+                      "executed_comparisons_per_pair": dense_exec / max((hi - lo) * Sd, 1),
+                      "pairs_per_s": (hi - lo) * Sd / dense_s, "sample": f"{hi - lo} region pairs x {Sd} samples"}
     # secondary: the focus-block GEMM (tensor-bound) and the sampled Pearson pairs (HBM/L2-bound)
     fa_box, fb_box = slabs[rank], fB
     nA = (fa_box[3] - fa_box[0]) * (fa_box[4] - fa_box[1]) * (fa_box[5] - fa_box[2])
@@ -399,7 +415,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, args, world),
-                "roofline": roofline, "roofline_pearson_block": roofline_block,
+                "roofline": roofline, "roofline_ksg_dense": roofline_dense, "roofline_pearson_block": roofline_block,
                 "roofline_pearson_pairs": roofline_pearson_pairs, "cpu_baseline": cpu_base, "e2e": e2e, "clocks": clk,
                 "gpu_launches": launches, "field_create_s": create_s,
                 "region_max_sample": [float(res[0][0]), int(res[1][0][0]), int(res[1][0][1])]}

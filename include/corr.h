@@ -45,7 +45,8 @@ typedef struct {
 enum { CORR_PEARSON = 0, CORR_KSG = 1 };
 enum {
   CORR_F_KSG_PLUS1 = 1 << 8, /* KSG with psi(n_x+1), psi(n_y+1) (Kraskov alg. 1; reading R1) */
-  CORR_F_ABS = 1 << 9        /* region max of |value| (reading R11)           */
+  CORR_F_ABS = 1 << 9,       /* region max of |value| (reading R11)           */
+  CORR_F_KSG_DENSE = 1 << 10 /* KSG: evaluate all n(n-1) comparisons (no exact sweep); same results */
 };
 enum { CORR_OK = 0, CORR_E_INVAL = -1, CORR_E_RANGE = -2, CORR_E_NOMEM = -3, CORR_E_CUDA = -4 };
 

@@ -115,6 +115,10 @@ int alloc_field(int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t dev
   return CORR_OK;
 }
 
+int ksg_flags(int32_t measure) {
+  return ((measure & CORR_F_KSG_PLUS1) ? 1 : 0) | ((measure & CORR_F_KSG_DENSE) ? 2 : 0);
+}
+
 int check_pair_fields(const corr_field* fa, const corr_field*& fb) {
   if (!fa) return fail(CORR_E_INVAL, "field is NULL");
   if (!fb) fb = fa;
@@ -126,7 +130,7 @@ int check_pair_fields(const corr_field* fa, const corr_field*& fb) {
 int resolve_k(const corr_field* f, int32_t measure, int32_t& k) {
   const int kind = measure & 0xFF;
   if (kind != CORR_PEARSON && kind != CORR_KSG) return fail(CORR_E_INVAL, "unknown measure kind");
-  if (measure & ~(0xFF | CORR_F_KSG_PLUS1 | CORR_F_ABS)) return fail(CORR_E_INVAL, "unknown measure flags");
+  if (measure & ~(0xFF | CORR_F_KSG_PLUS1 | CORR_F_ABS | CORR_F_KSG_DENSE)) return fail(CORR_E_INVAL, "unknown measure flags");
   if (kind == CORR_PEARSON) {
     k = 0;
     return CORR_OK;
@@ -299,7 +303,7 @@ static int eval_pairs_impl(const corr_field* fa, const corr_field* fb, int32_t m
   cudaStream_t st = (cudaStream_t)cuda_stream;
   cudaError_t e;
   if ((measure & 0xFF) == CORR_KSG) {
-    e = launch_ksg(fa, fb, k, (measure & CORR_F_KSG_PLUS1) != 0, src, po, st);
+    e = launch_ksg(fa, fb, k, ksg_flags(measure), src, po, st);
     if (e == cudaErrorNotSupported) return fail(CORR_E_INVAL, "KSG with k > 32 is not supported");
   } else {
     e = launch_pearson_pairs(fa, fb, src, po, st);
@@ -391,7 +395,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
   po.absval = (measure & CORR_F_ABS) != 0;
   if (e == cudaSuccess) {
     if ((measure & 0xFF) == CORR_KSG) {
-      e = launch_ksg(fa, fb, k, (measure & CORR_F_KSG_PLUS1) != 0, src, po, st);
+      e = launch_ksg(fa, fb, k, ksg_flags(measure), src, po, st);
       if (e == cudaErrorNotSupported) {
         cudaFreeAsync(dreg, st);
         cudaFreeAsync(keys, st);

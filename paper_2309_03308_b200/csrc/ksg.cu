@@ -259,7 +259,7 @@ cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, 256, smem, st>>>(fa->F, fb->F, fa->S, fb->S, fa->cflag, fb->cflag, fa->psi, n,
-                                              n_pad, k, plus1, src, out);
+                                              n_pad, k, plus1 & 1, src, out);
     note_launch();
   } else {
     auto kern = ksg_kernel<K, 8>;
@@ -275,7 +275,7 @@ cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, warps * 32, smem, st>>>(fa->F, fb->F, fa->S, fb->S, fa->cflag, fb->cflag, fa->psi,
-                                                     n, n_pad, k, plus1, src, out);
+                                                     n, n_pad, k, plus1 & 1, src, out);
     note_launch();
   }
   return cudaGetLastError();

@@ -379,7 +379,7 @@ cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus
   const int64_t cap = (int64_t)kSMs * occ;
   if (blocks > cap) blocks = cap;
   kern<<<(unsigned)blocks, warps * 32, smem, st>>>(fa->S, fa->perm, fa->F, fb->S, fb->perm, fb->F, fa->spread,
-                                                   fb->spread, fa->cflag, fb->cflag, fa->psi, n, n_pad, k, plus1,
+                                                   fb->spread, fa->cflag, fb->cflag, fa->psi, n, n_pad, k, plus1 & 1,
                                                    src, out);
   note_launch();
   return cudaGetLastError();
@@ -395,7 +395,9 @@ cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus
                      const PairOut& out, cudaStream_t st) {
   // CORR_KSG_SWEEP=0 disables the exact sweep (dense n(n-1) comparisons); CORR_KSG_RM picks
   // members per lane (1, 2 or 4) and CORR_KSG_G the filter group (4, or 8 with RM = 1).
-  static const int sweep = env_int("CORR_KSG_SWEEP", 1);
+  // plus1 bit 1 = CORR_F_KSG_DENSE: disable the exact sweep for this call
+  static const int sweep_env = env_int("CORR_KSG_SWEEP", 1);
+  const int sweep = sweep_env && !(plus1 & 2);
   static const int rm = env_int("CORR_KSG_RM", 1);
   static const int g = env_int("CORR_KSG_G", 4);
 #define CORR_KSG_CASE(RMv, Gv)                                                 \
@@ -428,7 +430,7 @@ cudaError_t launch_ksg_sorted(const corr_field* fa, const corr_field* fb, int k,
   // NEXT #2 (paper default k = ceil(3n/100)): register lists of 12/16/24/32;
   // inserting d >= l[KT-1] >= l[k-1] cannot change the k smallest, so the filter and the sweep
   // stay exact with the longer list, and eps = l[k-1].
-  const bool sweep = env_int("CORR_KSG_SWEEP", 1) != 0;
+  const bool sweep = env_int("CORR_KSG_SWEEP", 1) != 0 && !(plus1 & 2);
   if (k <= 12) return sweep ? launch_t<12, 1, 4, true>(fa, fb, k, plus1, src, out, st)
                             : launch_t<12, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   if (k <= 16) return sweep ? launch_t<16, 1, 4, true>(fa, fb, k, plus1, src, out, st)

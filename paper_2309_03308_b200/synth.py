@@ -222,6 +222,27 @@ def matrix_pairs(boxes: Sequence[Box]):
     return A, B
 
 
+def refine(box: Box, max_children: int) -> List[Box]:
+    """Focus-view refinement of a brick ("each brick is recursively refined into M/2
+    bricks"; SPEC.md:123 reading: halve every axis whose extent allows, octree-like, while the child
+    count stays <= max_children).  Children ordered x fastest."""
+    x0, y0, z0, x1, y1, z1 = box
+    parts = [1, 1, 1]
+    while True:
+        trial = [p * 2 if ((x1 - x0, y1 - y0, z1 - z0)[i] // (p * 2)) >= 1 else p for i, p in enumerate(parts)]
+        if trial == parts or trial[0] * trial[1] * trial[2] > max_children:
+            break
+        parts = trial
+    out = []
+    ext = (x1 - x0, y1 - y0, z1 - z0)
+    cuts = [[lo + ext[i] * c // parts[i] for c in range(parts[i] + 1)] for i, lo in enumerate((x0, y0, z0))]
+    for k in range(parts[2]):
+        for j in range(parts[1]):
+            for i in range(parts[0]):
+                out.append((cuts[0][i], cuts[1][j], cuts[2][k], cuts[0][i + 1], cuts[1][j + 1], cuts[2][k + 1]))
+    return out
+
+
 def box_size(b: Box) -> int:
     return (b[3] - b[0]) * (b[4] - b[1]) * (b[5] - b[2])
 

@@ -291,6 +291,38 @@ def test_pearson_block_n1000_and_two_fields():
     _block_compare(fa, None, ha, None, (sa.nx, sa.ny, sa.nz), A, B)
 
 
+def test_dense_and_sweep_identical():
+    """The exact sweep (default) and CORR_F_KSG_DENSE give bit-identical results."""
+    spec = synth.spec_of(synth.C4)
+    vals, f = _field(spec)
+    del vals
+    A, B = synth.context_pairs(synth.bricks_of(synth.C4))
+    A, B = A[::40], B[::40]
+    for k in (3, 30):
+        m1, a1 = cb.corr_region_max(f, None, cb.CORR_KSG, k, A, B, 8, 5)
+        m2, a2 = cb.corr_region_max(f, None, cb.CORR_KSG | cb.CORR_F_KSG_DENSE, k, A, B, 8, 5)
+        assert torch.equal(m1, m2) and torch.equal(a1, a2)
+    f.close()
+
+
+def test_focus_sub_brick_matrix():
+    """NEXT #3: the (M/2)^2 focus matrix of sub-brick pair maxima in one call; the
+    sub-bricks partition the parent bricks, so the matrix max is the parent pair max (same pair)."""
+    spec = synth.spec_of(synth.C2)
+    vals, f = _field(spec)
+    host = vals.cpu().numpy()
+    kids_a, kids_b = synth.refine(synth.C2_REGION_A, 44), synth.refine(synth.C2_REGION_B, 44)
+    assert len(kids_a) == 8 and sum(synth.box_size(b) for b in kids_a) == synth.box_size(synth.C2_REGION_A)
+    A = [a for a in kids_a for _ in kids_b]
+    B = [b for _ in kids_a for b in kids_b]
+    sm, sa = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, A, B, 0, 0)
+    pm, pa = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, [synth.C2_REGION_A], [synth.C2_REGION_B], 0, 0)
+    assert float(sm.max()) == float(pm[0])
+    for r in (0, 9, 63):
+        v, ab = oracle.pearson_block_max(host, None, (spec.nx, spec.ny, spec.nz), A[r], B[r])
+        assert abs(float(sm[r]) - v) <= PEARSON_TOL
+
+
 @pytest.mark.parametrize("fac", [(2, 2, 2), (4, 4, 4), (3, 2, 5)])
 def test_mean_tree_aggregate(fac):
     """NEXT #4: block means on the GPU equal the oracle's, and region maxima
