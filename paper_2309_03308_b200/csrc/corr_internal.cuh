@@ -71,11 +71,9 @@ struct PairOut {
 // ---- launchers (defined in the .cu files) ----
 cudaError_t launch_field_ingest(corr_field* f, const float* dvalues_member_major, cudaStream_t st);
 cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int fx, int fy, int fz, cudaStream_t st);
+// plus1: bit 0 = psi(n+1) variant, bit 1 = dense (no sweep)
 cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1,
                        const PairSrc& src, const PairOut& out, cudaStream_t st);
-// n > 128 members: x-sorted / filtered / sweep kernel (ksg_sorted.cu)
-cudaError_t launch_ksg_sorted(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
-                              const PairOut& out, cudaStream_t st);
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset);
 cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
                                  const PairOut& out, cudaStream_t st);

@@ -1,32 +1,40 @@
-// ksg.cu -- Kraskov (KSG) mutual information for batches of point pairs,
-// SURVEY.md §8(a) rows a2-a5 (+ a8/a9 when fed by the region sampler).
+// ksg.cu -- Kraskov (KSG) MI for batches of point pairs: sorted, filtered, exact sweep.
+// SURVEY.md §8(a) rows a2-a5 (+ a8/a9 via the pair source); NEXT #1 of §8(f).
 //
-// PAPER.md:172-174 (§3.2): for the joint samples z_i = (x_i, y_i), i = 1..n,
-//   eps_i  = Chebyshev distance to the k-th nearest neighbour (j != i),
-//   n_x,i  = #{ j : |x_i - x_j| < eps_i },  n_y,i likewise (strict),
-//   MI     = psi(n) + psi(k) - (1/n) sum_i [ psi(n_x,i) + psi(n_y,i) ]   (reading R2)
-// with fp32 distances (reading R7) so that eps and the counts are bit-identical to
-// the oracle's brute force.
+// Definitions (readings R1-R7): eps_i = k-th smallest Chebyshev distance
+// (fp32), strict marginal counts, MI = psi(n) + psi(k) - (1/n) sum_i [psi(n_x,i) + psi(n_y,i)].
 //
-// B200 design: the paper builds one k-d tree per pair in one
-// thread.  Here a team of warps owns one pair; each lane owns R = 4
-// members ("register blocking": one broadcast LDS.128 of two joint samples feeds
-// 8 comparisons) and keeps its k smallest distances in a sorted register list updated
-// by a branch-free min/max network (2k-1 FMNMX per comparison, no divergence).  The
-// self pair is excluded only on the diagonal 32-member chunks.  Marginal counts are
-// two binary searches per marginal on the field's pre-sorted rows with monotone fp32
-// predicates (bit-exact, O(log n) instead of the O(n) brute-force count).  psi comes
-// from a shared-memory fp64 table (arguments are integers; reading R17).
+// Measured facts that shape this kernel: FMNMX/FSETP issue on the ALU pipe at
+// 0.5 warp-instr/clk/SMSP (ncu: ALU 89 % busy at IPC 2.27 for the plain register network);
+// FMNMX3 costs the same slot for twice the work; FADD2 runs on the FMA pipe.  So the kernel
+// minimises ALU work per comparison:
+//  * the pair is staged sorted along its WIDER marginal (spread = ||x - mean||): the k-NN of a
+//    member then lies in a narrow window of that order.  KSG is symmetric in (x, y) (Eq. 1), so
+//    swapping the roles of a and b leaves eps unchanged and swaps the two counts (exact);
+//  * xy[t] = (S_u[t], F_v[perm_u[t]]) -- a member permutation; eps is order-free (R4);
+//  * a warp owns 32*RM sort-consecutive members (RM per lane: one broadcast LDS.128 of two
+//    joint samples feeds 2*RM comparisons); it scans its own block first (exact merge network,
+//    the j == i mask only on the diagonal member of each chunk), then 32-wide chunks outward;
+//  * outside the own block, per group of 4 j and member: 4 distances (FADD2 + FMNMX|.|), their
+//    min (FMNMX3 + FMNMX) and one compare with the list's k-th entry; only if some lane can
+//    insert (VOTE.ANY) does the warp run the exact merge network
+//        l'_r = min(l_r, max(l_{r-1}, a), max(l_{r-2}, b)),  (a, b) = sorted pair of new values
+//    -- inserting d >= l[K-1] is a no-op, so skipping it is exact;
+//  * SWEEP: a direction stops once fl(x_block_edge - x_chunk_edge) >= every member's current
+//    k-th distance: |fl(x_i - x_j)| >= that gap for all remaining j (monotone rounding), so no
+//    remaining j can enter any list (exact).  Executed comparisons are counted for the roofline;
+//  * counts: two binary searches per marginal on the sorted rows with monotone fp32
+//    predicates (bit-exact), psi from an fp64 shared table, fixed-order fp64 reduction.
 #include <math.h>
 #include <stdlib.h>
 
 #include "sampler.cuh"
 
 namespace corr {
-namespace {
 
-constexpr int R = 4;            // members per lane
-constexpr int kBlockMembers = 32 * R;
+__device__ unsigned long long g_ksg_comparisons;  // executed comparisons (corr_ksg_comparisons)
+
+namespace {
 
 __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
   unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a);
@@ -36,193 +44,311 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
   return *reinterpret_cast<float2*>(&ud);
 }
 
+__device__ __forceinline__ float cheb(float2 zi, float2 zj) {
+  const float2 d = sub2(zi, zj);
+  return fmaxf(fabsf(d.x), fabsf(d.y));
+}
+
 template <int K>
-__device__ __forceinline__ void knn_insert(float (&l)[K], float d) {
+__device__ __forceinline__ void merge2(float (&l)[K], float d0, float d1) {
+  const float a = fminf(d0, d1), b = fmaxf(d0, d1);
+  float nl[K];
+  nl[0] = fminf(l[0], a);
+  if (K >= 2) nl[1] = fminf(fminf(l[1], fmaxf(l[0], a)), b);
+#pragma unroll
+  for (int r = 2; r < K; ++r) nl[r] = fminf(fminf(l[r], fmaxf(l[r - 1], a)), fmaxf(l[r - 2], b));
+#pragma unroll
+  for (int r = 0; r < K; ++r) l[r] = nl[r];
+}
+
+// Strict marginal count of a member with value v and radius e on a sorted
+// array S (element stride ST): #{j != i : |fl(v - S_j)| < e}.
+//   e == 0: the strict interval is empty -> 0 (reading R5).
+//   e  > 0: u = first s with fl(s - v) >= e, w = first s with fl(v - s) < e (both predicates
+//           are monotone in s by monotone rounding, and imply / cover s >= v because e > 0);
+//           [w, u) holds every s with |fl(s - v)| < e, the member itself included -> u - w - 1.
+// Branch-free lower bounds (uniform trip count), the two searches interleaved for ILP.
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+template <int ST>
+__device__ __forceinline__ int marginal_count(const float* __restrict__ S, int n, float v, float e) {
+  if (!(e > 0.f)) return 0;
+  // 32-bit shared-memory byte addresses: one IADD + one SEL per probe and search
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(S);
+  uint32_t au = base, aw = base;
+  int len = n;
+  while (len > 1) {
+    const int half = len >> 1;
+    const uint32_t step = (uint32_t)(half * ST * 4);
+    const float su = lds_f32(au + step - ST * 4);
+    const float sw = lds_f32(aw + step - ST * 4);
+    au = (su - v >= e) ? au : au + step;   // not yet P_u -> move right
+    aw = (v - sw < e) ? aw : aw + step;    // not yet P_w -> move right
+    len -= half;
+  }
+  const int bu = (int)((au - base) / (ST * 4)), bw = (int)((aw - base) / (ST * 4));
+  const int u = bu + ((lds_f32(au) - v >= e) ? 0 : 1);
+  const int w = bw + ((v - lds_f32(aw) < e) ? 0 : 1);
+  return u - w - 1;
+}
+
+// own-block chunk: exact network; the self pair j == i exists only for member RC of each lane
+template <int K, int RM, int RC>
+__device__ __forceinline__ void own_chunk(const float4* __restrict__ cp, const float2 (&zi)[RM],
+                                          float (&l)[RM][K], int lane) {
+#pragma unroll 4
+  for (int h = 0; h < 16; ++h) {
+    const float4 v = cp[h];
+    const float2 z0 = make_float2(v.x, v.y), z1 = make_float2(v.z, v.w);
+#pragma unroll
+    for (int rr = 0; rr < RM; ++rr) {
+      float e0 = cheb(zi[rr], z0), e1 = cheb(zi[rr], z1);
+      if (rr == RC) {
+        if (2 * h == lane) e0 = INFINITY;
+        if (2 * h + 1 == lane) e1 = INFINITY;
+      }
+      merge2<K>(l[rr], e0, e1);
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void insert1(float (&l)[K], float d) {
 #pragma unroll
   for (int t = K - 1; t >= 1; --t) l[t] = fminf(l[t], fmaxf(l[t - 1], d));
   l[0] = fminf(l[0], d);
 }
 
-// strict marginal count, on the sorted row S[0..n):
-//   u = first t with S[t] >= v && fl(S[t]-v) >= e ;  w = first t with S[t] >= v || fl(v-S[t]) < e
-//   count = (u - w) - [e > 0]   (the self sample is inside [w, u) iff e > 0)
-__device__ __forceinline__ int marginal_count(const float* __restrict__ S, int n, float v, float e) {
-  int lo = 0, len = n;
-  while (len > 0) {
-    const int half = len >> 1;
-    const float s = S[lo + half];
-    const bool pred = (s >= v) && (s - v >= e);
-    if (pred) len = half; else { lo += half + 1; len -= half + 1; }
-  }
-  const int u = lo;
-  lo = 0; len = n;
-  while (len > 0) {
-    const int half = len >> 1;
-    const float s = S[lo + half];
-    const bool pred = (s >= v) || (v - s < e);
-    if (pred) len = half; else { lo += half + 1; len -= half + 1; }
-  }
-  return (u - lo) - (e > 0.f ? 1 : 0);
+// RM == 1 own chunk without masks: lane L reads the warp's 32 joint samples rotated by L
+// (a private doubled copy, dup[i] = chunk[i & 31]); s = 1..31 visits every j != i exactly once.
+template <int K>
+__device__ __forceinline__ void own_rotated(const float2* __restrict__ dup, int lane, float2 zi, float (&l)[K]) {
+  const float2* p = dup + lane;
+#pragma unroll
+  for (int s = 1; s < 31; s += 2) merge2<K>(l, cheb(zi, p[s]), cheb(zi, p[s + 1]));
+  insert1<K>(l, cheb(zi, p[31]));
 }
 
-// Team = one warp (TEAM_WARPS == 1, eight independent teams per CTA) or the whole CTA.
-template <int TEAM_WARPS>
-__device__ __forceinline__ void team_sync() {
-  if (TEAM_WARPS == 1) __syncwarp(); else __syncthreads();
+template <int K, int RM, int RC>
+struct OwnBlock {
+  __device__ __forceinline__ static void run(const float4* xy4, int c0, int nch, const float2 (&zi)[RM],
+                                             float (&l)[RM][K], int lane) {
+    OwnBlock<K, RM, RC - 1>::run(xy4, c0, nch, zi, l, lane);
+    if (c0 + RC < nch) own_chunk<K, RM, RC>(xy4 + (c0 + RC) * 16, zi, l, lane);
+  }
+};
+template <int K, int RM>
+struct OwnBlock<K, RM, -1> {
+  __device__ __forceinline__ static void run(const float4*, int, int, const float2 (&)[RM], float (&)[RM][K], int) {}
+};
+
+// one filtered 32-j chunk, groups of G j's (G = 4 or 8) per vote
+template <int K, int RM, int G, bool DESC>
+__device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
+                                               float (&l)[RM][K]) {
+  constexpr int NG = 32 / G;
+#pragma unroll 2
+  for (int gi = 0; gi < NG; ++gi) {
+    const int g = DESC ? NG - 1 - gi : gi;
+    float2 z[G];
+#pragma unroll
+    for (int q = 0; q < G / 2; ++q) {
+      const float4 v = cp[g * (G / 2) + q];
+      z[2 * q] = make_float2(v.x, v.y);
+      z[2 * q + 1] = make_float2(v.z, v.w);
+    }
+    float d[RM][G];
+    bool p = false;
+#pragma unroll
+    for (int rr = 0; rr < RM; ++rr) {
+#pragma unroll
+      for (int q = 0; q < G; ++q) d[rr][q] = cheb(zi[rr], z[q]);
+      float m = d[rr][0];
+#pragma unroll
+      for (int q = 1; q < G; ++q) m = fminf(m, d[rr][q]);
+      p |= m < l[rr][K - 1];
+    }
+    if (__any_sync(0xffffffffu, p)) {
+#pragma unroll
+      for (int rr = 0; rr < RM; ++rr) {
+#pragma unroll
+        for (int q = 0; q < G; q += 2) merge2<K>(l[rr], d[rr][q], d[rr][q + 1]);
+      }
+    }
+  }
 }
 
-template <int K, int TEAM_WARPS>
-__global__ void __launch_bounds__(256) ksg_kernel(const float* __restrict__ Fa, const float* __restrict__ Fb,
-                                                  const float* __restrict__ Sa, const float* __restrict__ Sb,
-                                                  const uint8_t* __restrict__ ca, const uint8_t* __restrict__ cb,
-                                                  const double* __restrict__ psi_g, int n, int n_pad, int k,
-                                                  int plus1, PairSrc src, PairOut out) {
+template <int K, int RM, int G, bool SWEEP>
+__global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sorted_kernel(
+    const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
+    const float* __restrict__ Sb, const uint16_t* __restrict__ Pb, const float* __restrict__ Fb,
+    const float* __restrict__ spa, const float* __restrict__ spb, const uint8_t* __restrict__ ca,
+    const uint8_t* __restrict__ cb, const double* __restrict__ psi_g, int n, int n_pad, int k, int plus1,
+    PairSrc src, PairOut out) {
+  constexpr int BLK = 32 * RM;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int kTeams = TEAM_WARPS == 1 ? 8 : 1;
-  const int warps_per_team = TEAM_WARPS == 1 ? 1 : (int)(blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int team = TEAM_WARPS == 1 ? warp : 0;
-  const int wt = TEAM_WARPS == 1 ? 0 : warp;  // warp index inside the team
-  const int tt = TEAM_WARPS == 1 ? lane : (int)threadIdx.x;
-  const int team_threads = 32 * warps_per_team;
-  const int nblk = (n + kBlockMembers - 1) / kBlockMembers;
-  const int nxy = nblk * kBlockMembers;  // joint samples staged, +inf padded
+  const int nwarps = blockDim.x >> 5;
+  const int nthreads = blockDim.x;
+  const int nblk = (n + BLK - 1) / BLK;
+  const int nxy = ((n + 127) / 128) * 128;
+  const int nch = (n + 31) >> 5;
 
   double* psi = reinterpret_cast<double*>(smem_raw);
   const int psi_len = (n + 2 + 1) & ~1;
-  unsigned char* team_base = smem_raw + psi_len * sizeof(double);
-  const size_t team_bytes = (size_t)nxy * sizeof(float2) + 2 * (size_t)n_pad * sizeof(float) + 32 * sizeof(double);
-  float2* xy = reinterpret_cast<float2*>(team_base + team * team_bytes);
-  float* sx = reinterpret_cast<float*>(xy + nxy);
-  float* sy = sx + n_pad;
-  double* red = reinterpret_cast<double*>(sy + n_pad);
+  float2* xy = reinterpret_cast<float2*>(smem_raw + psi_len * sizeof(double));
+  float* sy = reinterpret_cast<float*>(xy + nxy);
+  float* tb = sy + n_pad;
+  uint16_t* pm = reinterpret_cast<uint16_t*>(tb + n_pad);
+  double* red = reinterpret_cast<double*>(pm + n_pad + 8);
+  int* next_blk = reinterpret_cast<int*>(red + 32);
+  float2* dupbuf = reinterpret_cast<float2*>(red + 34);  // [8 warps][64] (RM == 1 own chunk)
 
-  for (int i = threadIdx.x; i < n + 2; i += blockDim.x) psi[i] = psi_g[i];
+  for (int i = threadIdx.x; i < n + 2; i += nthreads) psi[i] = psi_g[i];
   __syncthreads();
-
   const double psi_nk = psi[n] + psi[k];
   const int off = plus1 ? 1 : 0;
-  const int64_t team_id = (int64_t)blockIdx.x * kTeams + team;
-  const int64_t team_stride = (int64_t)gridDim.x * kTeams;
+  unsigned long long executed = 0;
 
-  for (int64_t u = team_id; u < src.nunits; u += team_stride) {
+  for (int64_t u = blockIdx.x; u < src.nunits; u += gridDim.x) {
     int64_t a, b, r;
     uint32_t idx;
     const bool ok = unit_pair(src, u, a, b, r, idx);
     if (!ok) {
-      if (src.mode == kList && tt == 0) out.out[u] = NAN;
+      if (src.mode == kList && threadIdx.x == 0) out.out[u] = NAN;
       continue;
     }
-    const bool degenerate = (ca[a] | cb[b]) != 0;  // constant series (reading R10)
+    const bool degenerate = (ca[a] | cb[b]) != 0;
     if (degenerate && out.dbg_eps == nullptr) {
-      if (src.mode == kList && tt == 0) out.out[u] = NAN;
+      if (src.mode == kList && threadIdx.x == 0) out.out[u] = NAN;
       continue;
     }
-    team_sync<TEAM_WARPS>();  // previous unit finished reading shared memory
-    // ---- a2: stage the pair (rows are 32-byte aligned) ----
-    {
-      const float4* fa4 = reinterpret_cast<const float4*>(Fa + a * n_pad);
-      const float4* fb4 = reinterpret_cast<const float4*>(Fb + b * n_pad);
-      const float4* sa4 = reinterpret_cast<const float4*>(Sa + a * n_pad);
-      const float4* sb4 = reinterpret_cast<const float4*>(Sb + b * n_pad);
-      float4* sx4 = reinterpret_cast<float4*>(sx);
-      float4* sy4 = reinterpret_cast<float4*>(sy);
-      for (int q = tt; q < n_pad / 4; q += team_threads) {
-        const float4 va = __ldg(fa4 + q), vb = __ldg(fb4 + q);
-        const int j = 4 * q;
-        float4* dst = reinterpret_cast<float4*>(xy + j);
-        const float inf = INFINITY;
-        dst[0] = make_float4(j + 0 < n ? va.x : inf, j + 0 < n ? vb.x : inf, j + 1 < n ? va.y : inf, j + 1 < n ? vb.y : inf);
-        dst[1] = make_float4(j + 2 < n ? va.z : inf, j + 2 < n ? vb.z : inf, j + 3 < n ? va.w : inf, j + 3 < n ? vb.w : inf);
-        sx4[q] = __ldg(sa4 + q);
-        sy4[q] = __ldg(sb4 + q);
-      }
-      for (int j = n_pad + tt; j < nxy; j += team_threads) xy[j] = make_float2(INFINITY, INFINITY);
+    // sort along the wider marginal (swap roles of x and y; exact by Eq. 1 symmetry)
+    const bool swap = spb[b] > spa[a];
+    const float* Su = swap ? Sb + b * n_pad : Sa + a * n_pad;
+    const uint16_t* Pu = swap ? Pb + b * n_pad : Pa + a * n_pad;
+    const float* Fv = swap ? Fa + a * n_pad : Fb + b * n_pad;
+    const float* Sv = swap ? Sa + a * n_pad : Sb + b * n_pad;
+    __syncthreads();
+    if (threadIdx.x == 0) *next_blk = nwarps;  // blocks 0..nwarps-1 are taken statically
+    // ---- a2: stage ----
+    for (int q = threadIdx.x; q < n_pad / 4; q += nthreads) {
+      reinterpret_cast<float4*>(tb)[q] = __ldg(reinterpret_cast<const float4*>(Fv) + q);
+      reinterpret_cast<float4*>(sy)[q] = __ldg(reinterpret_cast<const float4*>(Sv) + q);
+      reinterpret_cast<uint2*>(pm)[q] = __ldg(reinterpret_cast<const uint2*>(Pu) + q);
     }
-    team_sync<TEAM_WARPS>();
+    __syncthreads();
+    for (int q = threadIdx.x; q < nxy / 4; q += nthreads) {
+      const int t = 4 * q;
+      float4 xs = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+      if (t < n_pad) xs = __ldg(reinterpret_cast<const float4*>(Su) + q);
+      float4* dst = reinterpret_cast<float4*>(xy + t);
+      const float inf = INFINITY;
+      dst[0] = make_float4(t + 0 < n ? xs.x : inf, t + 0 < n ? tb[pm[t + 0]] : inf, t + 1 < n ? xs.y : inf,
+                           t + 1 < n ? tb[pm[t + 1]] : inf);
+      dst[1] = make_float4(t + 2 < n ? xs.z : inf, t + 2 < n ? tb[pm[t + 2]] : inf, t + 3 < n ? xs.w : inf,
+                           t + 3 < n ? tb[pm[t + 3]] : inf);
+    }
+    __syncthreads();
 
-    // ---- a3: k-NN pass; a4: counts; a5: psi terms ----
+    // ---- a3 / a4 / a5 ----
+    const float4* xy4 = reinterpret_cast<const float4*>(xy);
     double acc = 0.0;
-    for (int mb = wt; mb < nblk; mb += warps_per_team) {
-      float2 zi[R];
-      float l[R][K];
-      int irow[R];
+    // member blocks: first one static, then dynamic (sweep lengths differ per block)
+    for (int mb = warp; mb < nblk;) {
+      float2 zi[RM];
+      float l[RM][K];
+      int ts[RM];
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        irow[rr] = mb * kBlockMembers + 32 * rr + lane;
-        zi[rr] = xy[irow[rr]];
+      for (int rr = 0; rr < RM; ++rr) {
+        ts[rr] = mb * BLK + 32 * rr + lane;
+        zi[rr] = xy[ts[rr]];
 #pragma unroll
         for (int t = 0; t < K; ++t) l[rr][t] = INFINITY;
       }
-      const float4* xy4 = reinterpret_cast<const float4*>(xy);
-      const int nch = (n + 31) >> 5;
-      for (int c = 0; c < nch; ++c) {
-        const float4* cp = xy4 + c * 16;
-        if ((c >> 2) != mb) {
-#pragma unroll 8
-          for (int t = 0; t < 16; ++t) {
-            const float4 v = cp[t];
-            const float2 z0 = make_float2(v.x, v.y), z1 = make_float2(v.z, v.w);
+      const int c0 = mb * RM;
+      const int c1 = min(c0 + RM, nch);
+      if constexpr (RM == 1) {
+        float2* dup = dupbuf + warp * 64;
+        const float2 zc = xy[c0 * 32 + lane];
+        dup[lane] = zc;
+        dup[lane + 32] = zc;
+        __syncwarp();
+        own_rotated<K>(dup, lane, zi[0], l[0]);
+        __syncwarp();
+      } else {
+        OwnBlock<K, RM, RM - 1>::run(xy4, c0, nch, zi, l, lane);
+      }
+      int nproc = c1 - c0;
+      int clo = c0 - 1, chi = c1;
+      const float xblk_lo = xy[mb * BLK].x;
+      const float xblk_hi = xy[min(n, (mb + 1) * BLK) - 1].x;
+      while (clo >= 0 || chi < nch) {
+        float tmax = 0.f;
+        if (SWEEP) {
 #pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-              const float2 d0 = sub2(zi[rr], z0);
-              const float2 d1 = sub2(zi[rr], z1);
-              knn_insert<K>(l[rr], fmaxf(fabsf(d0.x), fabsf(d0.y)));
-              knn_insert<K>(l[rr], fmaxf(fabsf(d1.x), fabsf(d1.y)));
-            }
+          for (int rr = 0; rr < RM; ++rr)
+            if (ts[rr] < n) tmax = fmaxf(tmax, l[rr][K - 1]);
+          tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+        }
+        if (clo >= 0) {
+          if (SWEEP && (xblk_lo - xy[clo * 32 + 31].x) >= tmax) {
+            clo = -1;
+          } else {
+            chunk_filtered<K, RM, G, true>(xy4 + clo * 16, zi, l);
+            --clo;
+            ++nproc;
           }
-        } else {  // diagonal chunk: skip j == i ("k-th nearest neighbor", reading R3)
-          const int jb = c * 32;
-#pragma unroll 4
-          for (int t = 0; t < 16; ++t) {
-            const float4 v = cp[t];
-            const float2 z0 = make_float2(v.x, v.y), z1 = make_float2(v.z, v.w);
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-              const float2 d0 = sub2(zi[rr], z0);
-              const float2 d1 = sub2(zi[rr], z1);
-              float e0 = fmaxf(fabsf(d0.x), fabsf(d0.y));
-              float e1 = fmaxf(fabsf(d1.x), fabsf(d1.y));
-              if (jb + 2 * t == irow[rr]) e0 = INFINITY;
-              if (jb + 2 * t + 1 == irow[rr]) e1 = INFINITY;
-              knn_insert<K>(l[rr], e0);
-              knn_insert<K>(l[rr], e1);
-            }
+        }
+        if (chi < nch) {
+          if (SWEEP && (xy[chi * 32].x - xblk_hi) >= tmax) {
+            chi = nch;
+          } else {
+            chunk_filtered<K, RM, G, false>(xy4 + chi * 16, zi, l);
+            ++chi;
+            ++nproc;
           }
         }
       }
+      const int valid = min(BLK, n - mb * BLK);
+      if (lane == 0) executed += (unsigned long long)nproc * 32ull * (unsigned long long)valid;
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        if (irow[rr] < n) {
-          const float e = l[rr][K - 1];
-          const int cx = marginal_count(sx, n, zi[rr].x, e);
-          const int cy = marginal_count(sy, n, zi[rr].y, e);
-          acc += psi[cx + off] + psi[cy + off];
+      for (int rr = 0; rr < RM; ++rr) {
+        if (ts[rr] < n) {
+          float e = l[rr][K - 1];
+          if (K > 8) {  // list longer than k: eps = l[k-1] (the K smallest are exact)
+#pragma unroll
+            for (int t = 0; t < K - 1; ++t)
+              if (t == k - 1) e = l[rr][t];
+          }
+          const int cu = marginal_count<2>(reinterpret_cast<const float*>(xy), n, zi[rr].x, e);
+          const int cv = marginal_count<1>(sy, n, zi[rr].y, e);
+          acc += psi[cu + off] + psi[cv + off];
           if (out.dbg_eps) {
-            out.dbg_eps[u * n + irow[rr]] = e;
-            out.dbg_nx[u * n + irow[rr]] = cx;
-            out.dbg_ny[u * n + irow[rr]] = cy;
+            const int m = pm[ts[rr]];
+            out.dbg_eps[u * n + m] = e;
+            out.dbg_nx[u * n + m] = swap ? cv : cu;
+            out.dbg_ny[u * n + m] = swap ? cu : cv;
           }
         }
       }
+      int nb = 0;
+      if (lane == 0) nb = atomicAdd(next_blk, 1);
+      mb = __shfl_sync(0xffffffffu, nb, 0);
     }
-    // ---- team reduction of the psi sum (fp64, fixed order) ----
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (TEAM_WARPS != 1) {
-      if (lane == 0) red[wt] = acc;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < warps_per_team; ++w) s += red[w];
-        red[31] = s;
-      }
-      __syncthreads();
-      acc = red[31];
-    }
-    if (tt == 0) {
-      const float mi = degenerate ? NAN : (float)(psi_nk - acc / (double)n);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < nwarps; ++w) s += red[w];
+      const float mi = degenerate ? NAN : (float)(psi_nk - s / (double)n);
       if (src.mode == kList) {
         out.out[u] = mi;
       } else if (!isnan(mi)) {
@@ -230,55 +356,60 @@ __global__ void __launch_bounds__(256) ksg_kernel(const float* __restrict__ Fa, 
       }
     }
   }
+  if (lane == 0 && executed) atomicAdd(&g_ksg_comparisons, executed);
+}
+
+template <int K, int RM, int G, bool SWEEP>
+cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
+                     const PairOut& out, cudaStream_t st) {
+  const int n = fa->n, n_pad = fa->n_pad;
+  const int nxy = ((n + 127) / 128) * 128;
+  const int nblk = (n + 32 * RM - 1) / (32 * RM);
+  const size_t smem = (size_t)((n + 2 + 1) & ~1) * sizeof(double) + (size_t)nxy * sizeof(float2) +
+                      2 * (size_t)n_pad * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
+                      34 * sizeof(double) + 8 * 64 * sizeof(float2);
+  auto kern = ksg_sorted_kernel<K, RM, G, SWEEP>;
+  const int warps = nblk < 8 ? nblk : 8;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);
+  if (occ < 1) occ = 1;
+  int64_t blocks = src.nunits;
+  const int64_t cap = (int64_t)kSMs * occ;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, warps * 32, smem, st>>>(fa->S, fa->perm, fa->F, fb->S, fb->perm, fb->F, fa->spread,
+                                                   fb->spread, fa->cflag, fb->cflag, fa->psi, n, n_pad, k, plus1 & 1,
+                                                   src, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s && *s ? atoi(s) : dflt;
 }
 
 template <int K>
 cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                      const PairOut& out, cudaStream_t st) {
-  static const int small_sorted = [] {
-    const char* s = getenv("CORR_KSG_SMALL");  // "warp" keeps the one-warp-per-pair kernel
-    return (s && s[0] == 'w') ? 0 : 1;
-  }();
-  if (fa->n > kBlockMembers || small_sorted || k > 8) return launch_ksg_sorted(fa, fb, k, plus1, src, out, st);
-  const int n = fa->n, n_pad = fa->n_pad;
-  const int nblk = (n + kBlockMembers - 1) / kBlockMembers;
-  const int nxy = nblk * kBlockMembers;
-  const size_t psi_bytes = (size_t)((n + 2 + 1) & ~1) * sizeof(double);
-  const size_t team_bytes = (size_t)nxy * sizeof(float2) + 2 * (size_t)n_pad * sizeof(float) + 32 * sizeof(double);
-  int dev_sms = kSMs;
-  if (n <= kBlockMembers) {
-    auto kern = ksg_kernel<K, 1>;
-    const size_t smem = psi_bytes + 8 * team_bytes;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
-    if (occ < 1) occ = 1;
-    int64_t blocks = (src.nunits + 7) / 8;
-    const int64_t cap = (int64_t)dev_sms * occ;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, 256, smem, st>>>(fa->F, fb->F, fa->S, fb->S, fa->cflag, fb->cflag, fa->psi, n,
-                                              n_pad, k, plus1 & 1, src, out);
-    note_launch();
-  } else {
-    auto kern = ksg_kernel<K, 8>;
-    const int warps = nblk < 8 ? nblk : 8;
-    const size_t smem = psi_bytes + team_bytes;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);
-    if (occ < 1) occ = 1;
-    int64_t blocks = src.nunits;
-    const int64_t cap = (int64_t)dev_sms * occ;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, warps * 32, smem, st>>>(fa->F, fb->F, fa->S, fb->S, fa->cflag, fb->cflag, fa->psi,
-                                                     n, n_pad, k, plus1 & 1, src, out);
-    note_launch();
-  }
-  return cudaGetLastError();
+  // CORR_KSG_SWEEP=0 disables the exact sweep (dense n(n-1) comparisons); CORR_KSG_RM picks
+  // members per lane (1, 2 or 4) and CORR_KSG_G the filter group (4, or 8 with RM = 1).
+  // plus1 bit 1 = CORR_F_KSG_DENSE: disable the exact sweep for this call
+  static const int sweep_env = env_int("CORR_KSG_SWEEP", 1);
+  const int sweep = sweep_env && !(plus1 & 2);
+  static const int rm = env_int("CORR_KSG_RM", 1);
+  static const int g = env_int("CORR_KSG_G", 4);
+#define CORR_KSG_CASE(RMv, Gv)                                                 \
+  if (rm == RMv && g == Gv)                                                   \
+    return sweep ? launch_t<K, RMv, Gv, true>(fa, fb, k, plus1, src, out, st) \
+                 : launch_t<K, RMv, Gv, false>(fa, fb, k, plus1, src, out, st);
+  CORR_KSG_CASE(1, 8)
+  CORR_KSG_CASE(2, 4)
+  CORR_KSG_CASE(4, 4)
+#undef CORR_KSG_CASE
+  return sweep ? launch_t<K, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+               : launch_t<K, 1, 4, false>(fa, fb, k, plus1, src, out, st);
 }
 
 }  // namespace
@@ -286,7 +417,6 @@ cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus
 cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                        const PairOut& out, cudaStream_t st) {
   if (src.nunits == 0) return cudaSuccess;
-  if (k > 8) return launch_ksg_sorted(fa, fb, k, plus1, src, out, st);
   switch (k) {
     case 1: return launch_k<1>(fa, fb, k, plus1, src, out, st);
     case 2: return launch_k<2>(fa, fb, k, plus1, src, out, st);
@@ -296,8 +426,30 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int pl
     case 6: return launch_k<6>(fa, fb, k, plus1, src, out, st);
     case 7: return launch_k<7>(fa, fb, k, plus1, src, out, st);
     case 8: return launch_k<8>(fa, fb, k, plus1, src, out, st);
-    default: return cudaErrorNotSupported;
+    default: break;
   }
+  // NEXT #2 (paper default k = ceil(3n/100)): register lists of 12/16/24/32;
+  // inserting d >= l[KT-1] >= l[k-1] cannot change the k smallest, so the filter and the sweep
+  // stay exact with the longer list, and eps = l[k-1].
+  const bool sweep = env_int("CORR_KSG_SWEEP", 1) != 0 && !(plus1 & 2);
+  if (k <= 12) return sweep ? launch_t<12, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<12, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  if (k <= 16) return sweep ? launch_t<16, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<16, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  if (k <= 24) return sweep ? launch_t<24, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<24, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  if (k <= 32) return sweep ? launch_t<32, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<32, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  return cudaErrorNotSupported;
+}
+
+cudaError_t ksg_comparisons(unsigned long long* value, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(value, g_ksg_comparisons, sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long zero = 0;
+    e = cudaMemcpyToSymbol(g_ksg_comparisons, &zero, sizeof(zero));
+  }
+  return e;
 }
 
 }  // namespace corr

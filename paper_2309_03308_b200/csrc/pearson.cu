@@ -13,31 +13,34 @@
 namespace corr {
 namespace {
 
+// LPP lanes per pair (4..32): small n packs several pairs into one warp so every lane keeps
+// loads in flight (one-to-all / sampled pairs are a latency-bound gather otherwise).
+template <int LPP>
 __global__ void __launch_bounds__(256) pearson_pairs_kernel(const float* __restrict__ Za, const float* __restrict__ Zb,
                                                             const uint8_t* __restrict__ ca,
                                                             const uint8_t* __restrict__ cb, int n_pad, PairSrc src,
                                                             PairOut out) {
+  constexpr int PPW = 32 / LPP;  // pairs per warp
   const int lane = threadIdx.x & 31;
+  const int sub = lane / LPP, sl = lane % LPP;
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = warp0; u < src.nunits; u += nwarps) {
-    int64_t a, b, r;
-    uint32_t idx;
-    const bool ok = unit_pair(src, u, a, b, r, idx);
-    if (!ok) {
-      if (src.mode == kList && lane == 0) out.out[u] = NAN;
-      continue;
-    }
-    float acc = 0.f;
-    if (!(ca[a] | cb[b])) {
+  const int nq = n_pad >> 2;
+  for (int64_t u0 = warp0 * PPW; u0 < src.nunits; u0 += nwarps * PPW) {
+    const int64_t u = u0 + sub;
+    int64_t a = 0, b = 0, r = 0;
+    uint32_t idx = 0;
+    const bool live = u < src.nunits;
+    const bool ok = live && unit_pair(src, u, a, b, r, idx);
+    const bool valid = ok && !(ca[a] | cb[b]);
+    float acc = 0.f, acc1 = 0.f;
+    if (valid) {
       const float4* pa = reinterpret_cast<const float4*>(Za + a * n_pad);
       const float4* pb = reinterpret_cast<const float4*>(Zb + b * n_pad);
-      const int nq = n_pad >> 2;
-      float acc1 = 0.f;
-      int q = lane;
-      for (; q + 32 < nq; q += 64) {
+      int q = sl;
+      for (; q + LPP < nq; q += 2 * LPP) {
         const float4 x0 = __ldg(pa + q), y0 = __ldg(pb + q);
-        const float4 x1 = __ldg(pa + q + 32), y1 = __ldg(pb + q + 32);
+        const float4 x1 = __ldg(pa + q + LPP), y1 = __ldg(pb + q + LPP);
         acc = fmaf(x0.x, y0.x, acc); acc = fmaf(x0.y, y0.y, acc);
         acc = fmaf(x0.z, y0.z, acc); acc = fmaf(x0.w, y0.w, acc);
         acc1 = fmaf(x1.x, y1.x, acc1); acc1 = fmaf(x1.y, y1.y, acc1);
@@ -48,18 +51,16 @@ __global__ void __launch_bounds__(256) pearson_pairs_kernel(const float* __restr
         acc = fmaf(x0.x, y0.x, acc); acc = fmaf(x0.y, y0.y, acc);
         acc = fmaf(x0.z, y0.z, acc); acc = fmaf(x0.w, y0.w, acc);
       }
-      acc += acc1;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      acc = fminf(1.f, fmaxf(-1.f, acc));
-    } else {
-      acc = NAN;
     }
-    if (lane == 0) {
+    acc += acc1;
+#pragma unroll
+    for (int o = LPP / 2; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (sl == 0 && live) {
+      const float v = valid ? fminf(1.f, fmaxf(-1.f, acc)) : NAN;
       if (src.mode == kList) {
-        out.out[u] = acc;
-      } else if (!isnan(acc)) {
-        atomicMax(out.keys + r, pack_key(out.absval ? fabsf(acc) : acc, idx));
+        out.out[u] = v;
+      } else if (valid) {
+        atomicMax(out.keys + r, pack_key(out.absval ? fabsf(v) : v, idx));
       }
     }
   }
@@ -98,13 +99,24 @@ __global__ void region_finalize_kernel(PairSrc src, const unsigned long long* __
 cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
                                  const PairOut& out, cudaStream_t st) {
   if (src.nunits == 0) return cudaSuccess;
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pearson_pairs_kernel, 256, 0);
-  if (occ < 1) occ = 1;
-  int64_t blocks = (src.nunits + 7) / 8;
-  const int64_t cap = (int64_t)kSMs * occ * 4;
-  if (blocks > cap) blocks = cap;
-  pearson_pairs_kernel<<<(unsigned)blocks, 256, 0, st>>>(fa->Z, fb->Z, fa->cflag, fb->cflag, fa->n_pad, src, out);
+  const int nq = fa->n_pad / 4;
+  int lpp = 4;
+  while (lpp < 32 && lpp * 4 < nq) lpp <<= 1;
+  auto launch = [&](auto kern, int ppw) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+    if (occ < 1) occ = 1;
+    int64_t blocks = (src.nunits + 8 * ppw - 1) / (8 * ppw);
+    const int64_t cap = (int64_t)kSMs * occ * 4;
+    if (blocks > cap) blocks = cap;
+    kern<<<(unsigned)blocks, 256, 0, st>>>(fa->Z, fb->Z, fa->cflag, fb->cflag, fa->n_pad, src, out);
+  };
+  switch (lpp) {
+    case 4: launch(pearson_pairs_kernel<4>, 8); break;
+    case 8: launch(pearson_pairs_kernel<8>, 4); break;
+    case 16: launch(pearson_pairs_kernel<16>, 2); break;
+    default: launch(pearson_pairs_kernel<32>, 1); break;
+  }
   note_launch();
   return cudaGetLastError();
 }
