@@ -14,7 +14,7 @@ from typing import Optional, Sequence, Tuple
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcorr.so")
+LIB_PATH = os.environ.get("CORR_LIB", os.path.join(_HERE, "libcorr.so"))  # override: A/B experiments
 
 CORR_PEARSON = 0
 CORR_KSG = 1

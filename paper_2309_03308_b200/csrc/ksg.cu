@@ -284,11 +284,14 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
       } else {
         OwnBlock<K, RM, RM - 1>::run(xy4, c0, nch, zi, l, lane);
       }
+      // outward in chunks of 32 j; below descending, above ascending
+      const int nh = nch;
+      int break_lo = -1, break_hi = nh;
       int nproc = c1 - c0;
-      int clo = c0 - 1, chi = c1;
+      int hlo = c0 - 1, hhi = c1;
       const float xblk_lo = xy[mb * BLK].x;
       const float xblk_hi = xy[min(n, (mb + 1) * BLK) - 1].x;
-      while (clo >= 0 || chi < nch) {
+      while (hlo >= 0 || hhi < nh) {
         float tmax = 0.f;
         if (SWEEP) {
 #pragma unroll
@@ -296,27 +299,31 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
             if (ts[rr] < n) tmax = fmaxf(tmax, l[rr][K - 1]);
           tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
         }
-        if (clo >= 0) {
-          if (SWEEP && (xblk_lo - xy[clo * 32 + 31].x) >= tmax) {
-            clo = -1;
+        if (hlo >= 0) {
+          if (SWEEP && (xblk_lo - xy[hlo * 32 + 31].x) >= tmax) {
+            break_lo = hlo;
+            hlo = -1;
           } else {
-            chunk_filtered<K, RM, G, true>(xy4 + clo * 16, zi, l);
-            --clo;
+            chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l);
+            --hlo;
             ++nproc;
           }
         }
-        if (chi < nch) {
-          if (SWEEP && (xy[chi * 32].x - xblk_hi) >= tmax) {
-            chi = nch;
+        if (hhi < nh) {
+          if (SWEEP && (xy[hhi * 32].x - xblk_hi) >= tmax) {
+            break_hi = hhi;
+            hhi = nh;
           } else {
-            chunk_filtered<K, RM, G, false>(xy4 + chi * 16, zi, l);
-            ++chi;
+            chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l);
+            ++hhi;
             ++nproc;
           }
         }
       }
       const int valid = min(BLK, n - mb * BLK);
       if (lane == 0) executed += (unsigned long long)nproc * 32ull * (unsigned long long)valid;
+      // the sorted-marginal strip |fl(x_j - x_i)| < eps_i lies inside the scanned window
+      const int wlo = 32 * (break_lo + 1), whi = min(n, 32 * break_hi);
 #pragma unroll
       for (int rr = 0; rr < RM; ++rr) {
         if (ts[rr] < n) {
@@ -326,7 +333,7 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
             for (int t = 0; t < K - 1; ++t)
               if (t == k - 1) e = l[rr][t];
           }
-          const int cu = marginal_count<2>(reinterpret_cast<const float*>(xy), n, zi[rr].x, e);
+          const int cu = marginal_count<2>(reinterpret_cast<const float*>(xy + wlo), whi - wlo, zi[rr].x, e);
           const int cv = marginal_count<1>(sy, n, zi[rr].y, e);
           acc += psi[cu + off] + psi[cv + off];
           if (out.dbg_eps) {
