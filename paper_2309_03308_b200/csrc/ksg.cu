@@ -289,18 +289,20 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
       int break_lo = -1, break_hi = nh;
       int nproc = c1 - c0;
       int hlo = c0 - 1, hhi = c1;
-      const float xblk_lo = xy[mb * BLK].x;
-      const float xblk_hi = xy[min(n, (mb + 1) * BLK) - 1].x;
       while (hlo >= 0 || hhi < nh) {
-        float tmax = 0.f;
-        if (SWEEP) {
-#pragma unroll
-          for (int rr = 0; rr < RM; ++rr)
-            if (ts[rr] < n) tmax = fmaxf(tmax, l[rr][K - 1]);
-          tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
-        }
+        // SWEEP: per-member exact test -- member i still needs the chunk iff the x-gap to the
+        // chunk's nearest edge is below its current k-th distance: fl(x_i - x_edge) < l_i[K-1]
+        // (below) or fl(x_edge - x_i) < l_i[K-1] (above).  Skip the direction once no lane does.
         if (hlo >= 0) {
-          if (SWEEP && (xblk_lo - xy[hlo * 32 + 31].x) >= tmax) {
+          bool need = true;
+          if (SWEEP) {
+            const float xe = xy[hlo * 32 + 31].x;
+            bool p = false;
+#pragma unroll
+            for (int rr = 0; rr < RM; ++rr) p |= (ts[rr] < n) && (zi[rr].x - xe < l[rr][K - 1]);
+            need = __any_sync(0xffffffffu, p);
+          }
+          if (!need) {
             break_lo = hlo;
             hlo = -1;
           } else {
@@ -310,7 +312,15 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
           }
         }
         if (hhi < nh) {
-          if (SWEEP && (xy[hhi * 32].x - xblk_hi) >= tmax) {
+          bool need = true;
+          if (SWEEP) {
+            const float xe = xy[hhi * 32].x;
+            bool p = false;
+#pragma unroll
+            for (int rr = 0; rr < RM; ++rr) p |= (ts[rr] < n) && (xe - zi[rr].x < l[rr][K - 1]);
+            need = __any_sync(0xffffffffu, p);
+          }
+          if (!need) {
             break_hi = hhi;
             hhi = nh;
           } else {
