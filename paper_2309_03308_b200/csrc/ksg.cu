@@ -28,6 +28,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "sampler.cuh"
 
 namespace corr {
@@ -74,26 +76,26 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   return v;
 }
 
+// Power-of-two steps over an array padded with +inf to 2^LOG2 > n entries (the padding
+// satisfies both predicates): pos = number of leading "not P" elements; every probe is an LDS
+// with an immediate offset, the step sequence is uniform across the warp.
 template <int ST>
-__device__ __forceinline__ int marginal_count(const float* __restrict__ S, int n, float v, float e) {
+__device__ __forceinline__ int marginal_count(const float* __restrict__ S, int log2p, float v, float e) {
   if (!(e > 0.f)) return 0;
-  // 32-bit shared-memory byte addresses: one IADD + one SEL per probe and search
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(S);
   uint32_t au = base, aw = base;
-  int len = n;
-  while (len > 1) {
-    const int half = len >> 1;
-    const uint32_t step = (uint32_t)(half * ST * 4);
-    const float su = lds_f32(au + step - ST * 4);
-    const float sw = lds_f32(aw + step - ST * 4);
-    au = (su - v >= e) ? au : au + step;   // not yet P_u -> move right
-    aw = (v - sw < e) ? aw : aw + step;    // not yet P_w -> move right
-    len -= half;
+#pragma unroll
+  for (int b = 13; b >= 0; --b) {
+    if (b < log2p) {
+      constexpr uint32_t kStride = ST * 4;
+      const uint32_t step = (1u << b) * kStride;
+      const float su = lds_f32(au + step - kStride);
+      const float sw = lds_f32(aw + step - kStride);
+      au = (su - v >= e) ? au : au + step;   // not yet P_u -> move right
+      aw = (v - sw < e) ? aw : aw + step;    // not yet P_w -> move right
+    }
   }
-  const int bu = (int)((au - base) / (ST * 4)), bw = (int)((aw - base) / (ST * 4));
-  const int u = bu + ((lds_f32(au) - v >= e) ? 0 : 1);
-  const int w = bw + ((v - lds_f32(aw) < e) ? 0 : 1);
-  return u - w - 1;
+  return (int)((au - aw) / (ST * 4)) - 1;
 }
 
 // own-block chunk: exact network; the self pair j == i exists only for member RC of each lane
@@ -196,14 +198,17 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
   const int nwarps = blockDim.x >> 5;
   const int nthreads = blockDim.x;
   const int nblk = (n + BLK - 1) / BLK;
-  const int nxy = ((n + 127) / 128) * 128;
+  int log2p = 1;
+  while ((1 << log2p) <= n) ++log2p;  // 2^log2p > n: +inf padded search arrays
+  const int nxy = max(((n + 127) / 128) * 128, 1 << log2p);
+  const int nsy = max(n_pad, 1 << log2p);
   const int nch = (n + 31) >> 5;
 
   double* psi = reinterpret_cast<double*>(smem_raw);
   const int psi_len = (n + 2 + 1) & ~1;
   float2* xy = reinterpret_cast<float2*>(smem_raw + psi_len * sizeof(double));
   float* sy = reinterpret_cast<float*>(xy + nxy);
-  float* tb = sy + n_pad;
+  float* tb = sy + nsy;
   uint16_t* pm = reinterpret_cast<uint16_t*>(tb + n_pad);
   double* red = reinterpret_cast<double*>(pm + n_pad + 8);
   int* next_blk = reinterpret_cast<int*>(red + 32);
@@ -242,6 +247,7 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
       reinterpret_cast<float4*>(sy)[q] = __ldg(reinterpret_cast<const float4*>(Sv) + q);
       reinterpret_cast<uint2*>(pm)[q] = __ldg(reinterpret_cast<const uint2*>(Pu) + q);
     }
+    for (int t = n_pad + threadIdx.x; t < nsy; t += nthreads) sy[t] = INFINITY;
     __syncthreads();
     for (int q = threadIdx.x; q < nxy / 4; q += nthreads) {
       const int t = 4 * q;
@@ -286,7 +292,6 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
       }
       // outward in chunks of 32 j; below descending, above ascending
       const int nh = nch;
-      int break_lo = -1, break_hi = nh;
       int nproc = c1 - c0;
       int hlo = c0 - 1, hhi = c1;
       while (hlo >= 0 || hhi < nh) {
@@ -303,7 +308,6 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
             need = __any_sync(0xffffffffu, p);
           }
           if (!need) {
-            break_lo = hlo;
             hlo = -1;
           } else {
             chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l);
@@ -321,7 +325,6 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
             need = __any_sync(0xffffffffu, p);
           }
           if (!need) {
-            break_hi = hhi;
             hhi = nh;
           } else {
             chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l);
@@ -332,8 +335,6 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
       }
       const int valid = min(BLK, n - mb * BLK);
       if (lane == 0) executed += (unsigned long long)nproc * 32ull * (unsigned long long)valid;
-      // the sorted-marginal strip |fl(x_j - x_i)| < eps_i lies inside the scanned window
-      const int wlo = 32 * (break_lo + 1), whi = min(n, 32 * break_hi);
 #pragma unroll
       for (int rr = 0; rr < RM; ++rr) {
         if (ts[rr] < n) {
@@ -343,8 +344,8 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
             for (int t = 0; t < K - 1; ++t)
               if (t == k - 1) e = l[rr][t];
           }
-          const int cu = marginal_count<2>(reinterpret_cast<const float*>(xy + wlo), whi - wlo, zi[rr].x, e);
-          const int cv = marginal_count<1>(sy, n, zi[rr].y, e);
+          const int cu = marginal_count<2>(reinterpret_cast<const float*>(xy), log2p, zi[rr].x, e);
+          const int cv = marginal_count<1>(sy, log2p, zi[rr].y, e);
           acc += psi[cu + off] + psi[cv + off];
           if (out.dbg_eps) {
             const int m = pm[ts[rr]];
@@ -380,10 +381,13 @@ template <int K, int RM, int G, bool SWEEP>
 cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                      const PairOut& out, cudaStream_t st) {
   const int n = fa->n, n_pad = fa->n_pad;
-  const int nxy = ((n + 127) / 128) * 128;
+  int log2p = 1;
+  while ((1 << log2p) <= n) ++log2p;
+  const int nxy = std::max(((n + 127) / 128) * 128, 1 << log2p);
+  const int nsy = std::max(n_pad, 1 << log2p);
   const int nblk = (n + 32 * RM - 1) / (32 * RM);
   const size_t smem = (size_t)((n + 2 + 1) & ~1) * sizeof(double) + (size_t)nxy * sizeof(float2) +
-                      2 * (size_t)n_pad * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
+                      (size_t)(nsy + n_pad) * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
                       34 * sizeof(double) + 8 * 64 * sizeof(float2);
   auto kern = ksg_sorted_kernel<K, RM, G, SWEEP>;
   const int warps = nblk < 8 ? nblk : 8;
