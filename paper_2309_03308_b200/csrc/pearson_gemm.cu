@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -352,6 +353,316 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================
+// 2-SM variant (cta_group::2): a cluster of two CTAs computes a 256 x 256 tile with one
+// M=256 N=256 tcgen05.mma per k-step issued by the leader CTA.  Each CTA stages its own
+// 128 A rows and its own 128 of the 256 B rows (the MMA reads the peer's halves at the same
+// shared-memory offsets), so every SM moves 2/3 of the operand bytes of the 1-SM kernel for
+// the same tensor work.  TMA completions of both CTAs land on the leader's full barrier
+// (peer bit cleared); MMA commits multicast to both CTAs' empty / accumulator barriers; both
+// epilogues release the leader's accumulator barrier.  Per CTA the epilogue is unchanged:
+// its 128 TMEM lanes are its 128 A rows, the 256 columns span both CTAs' B halves.
+// ============================================================================
+constexpr int STAGES2 = 3;
+constexpr int H_BYTES = 128 * BK * 4;            // one 128-row plane of one k-block: 16 KB
+constexpr int STAGE2_BYTES = 4 * H_BYTES;        // A_hi, A_lo, B_hi, B_lo halves: 64 KB
+constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+
+struct Gemm2Region {
+  corr_box A, B;
+  int ntA[3], ntB[3];   // 128-row tiles along x, y, z
+  int64_t nta, ntb;     // 128-row tiles per box
+  int64_t tile_off;     // prefix of cluster tiles ceil(nta/2) * ceil(ntb/2)
+  int64_t nA, nB;
+  int overlap;
+  int pad;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                int c2, int c3) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;  // peer bit cleared: the leader's barrier
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void tc_commit_2sm(uint64_t* bar) {
+  const uint16_t mask = 0x3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void tile_xyz(const int (&nt)[3], int64_t t, int& tx, int& ty, int& tz) {
+  tx = (int)(t % nt[0]);
+  ty = (int)((t / nt[0]) % nt[1]);
+  tz = (int)(t / ((int64_t)nt[0] * nt[1]));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    pearson_block2_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                          const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                          const Gemm2Region* __restrict__ reg, GemmGeom g, const uint8_t* __restrict__ ca,
+                          const uint8_t* __restrict__ cb, unsigned long long* __restrict__ keys) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* stage_base = base;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES2 * STAGE2_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* colbias = reinterpret_cast<float*>(tmem_slot + 4);  // [2][256]
+  int* colpt = reinterpret_cast<int*>(colbias + 2 * BN);      // [2][256]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(full + s, 2);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto coord = [&](int64_t t, int64_t& r, int64_t& mi, int64_t& ni) {
+    int64_t lo = 0, hi = g.nreg - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (reg[mid].tile_off <= t) lo = mid; else hi = mid - 1;
+    }
+    r = lo;
+    const int64_t mb = (reg[lo].ntb + 1) >> 1;
+    const int64_t q = t - reg[lo].tile_off;
+    mi = q / mb;
+    ni = q - mi * mb;
+  };
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mAhi) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mAlo) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mBhi) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mBlo) : "memory");
+      uint32_t it = 0;
+      for (int64_t t = cid; t < g.total_tiles; t += ncl) {
+        int64_t r, mi, ni;
+        coord(t, r, mi, ni);
+        const Gemm2Region& R = reg[r];
+        int64_t ta = 2 * mi + rank, tb = 2 * ni + rank;
+        if (ta >= R.nta) ta = R.nta - 1;  // odd tail: any valid tile, rows masked in the epilogue
+        if (tb >= R.ntb) tb = R.ntb - 1;
+        int tx, ty, tz, ux, uy, uz;
+        tile_xyz(R.ntA, ta, tx, ty, tz);
+        tile_xyz(R.ntB, tb, ux, uy, uz);
+        const int ax = R.A.x0 + tx * g.bxA, ay = R.A.y0 + ty * g.byA, az = R.A.z0 + tz * g.bzA;
+        const int bx = R.B.x0 + ux * g.bxB, by = R.B.y0 + uy * g.byB, bz = R.B.z0 + uz * g.bzB;
+        for (int kb = 0; kb < g.kblocks; ++kb, ++it) {
+          const uint32_t s = it % STAGES2, ph = (it / STAGES2) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          if (rank == 0) mbar_expect_tx(full + s, 2 * STAGE2_BYTES);
+          else mbar_arrive_cluster(mapa_rank(smem_u32(full + s), 0));
+          unsigned char* st = stage_base + s * STAGE2_BYTES;
+          tma_load_4d_2sm(st, &mAhi, full + s, kb * BK, ax, ay, az);
+          tma_load_4d_2sm(st + H_BYTES, &mAlo, full + s, kb * BK, ax, ay, az);
+          tma_load_4d_2sm(st + 2 * H_BYTES, &mBhi, full + s, kb * BK, bx, by, bz);
+          tma_load_4d_2sm(st + 3 * H_BYTES, &mBlo, full + s, kb * BK, bx, by, bz);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (rank == 0) {
+      uint32_t it = 0, tt = 0;
+      for (int64_t t = cid; t < g.total_tiles; t += ncl, ++tt) {
+        const uint32_t acc = tt & 1, aph = (tt >> 1) & 1;
+        mbar_wait(tempty + acc, aph ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + acc * BN;
+        for (int kb = 0; kb < g.kblocks; ++kb, ++it) {
+          const uint32_t s = it % STAGES2, ph = (it / STAGES2) & 1;
+          mbar_wait(full + s, ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t st = smem_u32(stage_base + s * STAGE2_BYTES);
+            const uint64_t dAhi = sdesc_sw128(st), dAlo = sdesc_sw128(st + H_BYTES);
+            const uint64_t dBhi = sdesc_sw128(st + 2 * H_BYTES), dBlo = sdesc_sw128(st + 3 * H_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+              const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
+              tc_mma_tf32_2sm(dcol, dAhi + adv, dBhi + adv, kIdesc2, first);
+              tc_mma_tf32_2sm(dcol, dAhi + adv, dBlo + adv, kIdesc2, 1u);
+              tc_mma_tf32_2sm(dcol, dAlo + adv, dBhi + adv, kIdesc2, 1u);
+            }
+            tc_commit_2sm(empty + s);
+          }
+          __syncwarp();
+        }
+        if (lane == 0) tc_commit_2sm(tfull + acc);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5 of both CTAs) =====================
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const int et = threadIdx.x - 64;
+    const uint32_t tempty_leader = mapa_rank(smem_u32(tempty), 0);
+    uint32_t tt = 0;
+    for (int64_t t = cid; t < g.total_tiles; t += ncl, ++tt) {
+      const uint32_t acc = tt & 1, aph = (tt >> 1) & 1;
+      int64_t r, mi, ni;
+      coord(t, r, mi, ni);
+      const Gemm2Region& R = reg[r];
+      float* cbias = colbias + acc * BN;
+      int* cpt = colpt + acc * BN;
+      for (int n = et; n < BN; n += 128) {
+        const int h = n >> 7, nr = n & 127;
+        const int64_t tb = 2 * ni + h;
+        bool ok = tb < R.ntb;
+        int p = -1;
+        if (ok) {
+          int ux, uy, uz;
+          tile_xyz(R.ntB, tb, ux, uy, uz);
+          const int lx = nr % g.bxB, ly = (nr / g.bxB) % g.byB, lz = nr / (g.bxB * g.byB);
+          const int x = R.B.x0 + ux * g.bxB + lx, y = R.B.y0 + uy * g.byB + ly, z = R.B.z0 + uz * g.bzB + lz;
+          ok = x < R.B.x1 && y < R.B.y1 && z < R.B.z1;
+          if (ok) {
+            p = (z * g.ny + y) * g.nx + x;
+            ok = cb[p] == 0;
+          }
+        }
+        cbias[n] = ok ? 0.f : -INFINITY;
+        cpt[n] = p;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int64_t ta = 2 * mi + rank;
+      bool row_ok = ta < R.nta;
+      int xa = 0, ya = 0, za = 0, pa = -1;
+      if (row_ok) {
+        int tx, ty, tz;
+        tile_xyz(R.ntA, ta, tx, ty, tz);
+        const int lxA = row % g.bxA, lyA = (row / g.bxA) % g.byA, lzA = row / (g.bxA * g.byA);
+        xa = R.A.x0 + tx * g.bxA + lxA;
+        ya = R.A.y0 + ty * g.byA + lyA;
+        za = R.A.z0 + tz * g.bzA + lzA;
+        row_ok = xa < R.A.x1 && ya < R.A.y1 && za < R.A.z1;
+        if (row_ok) {
+          pa = (za * g.ny + ya) * g.nx + xa;
+          row_ok = ca[pa] == 0;
+        }
+      }
+      const bool selfmask = R.overlap != 0;
+      mbar_wait(tfull + acc, aph);
+      tc_fence_after();
+      float best = -INFINITY;
+      int bidx = 0;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q4 * 32) << 16);
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        float v[32];
+        tmem_ld32(taddr + ch * 32, v);
+        const float4* b4 = reinterpret_cast<const float4*>(cbias + ch * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 bb = b4[i];
+          v[4 * i + 0] = (g.absval ? fabsf(v[4 * i + 0]) : v[4 * i + 0]) + bb.x;
+          v[4 * i + 1] = (g.absval ? fabsf(v[4 * i + 1]) : v[4 * i + 1]) + bb.y;
+          v[4 * i + 2] = (g.absval ? fabsf(v[4 * i + 2]) : v[4 * i + 2]) + bb.z;
+          v[4 * i + 3] = (g.absval ? fabsf(v[4 * i + 3]) : v[4 * i + 3]) + bb.w;
+        }
+        if (selfmask) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (cpt[ch * 32 + i] == pa) v[i] = -INFINITY;
+        }
+        float m = v[0];
+#pragma unroll
+        for (int i = 1; i < 32; ++i) m = fmaxf(m, v[i]);
+        if (m > best) {
+          int j = 31;
+#pragma unroll
+          for (int i = 31; i >= 0; --i)
+            if (v[i] == m) j = i;
+          best = m;
+          bidx = ch * 32 + j;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+      unsigned long long key = 0ULL;
+      if (row_ok && best > -INFINITY) {
+        best = fminf(1.f, fmaxf(-1.f, best));
+        const int pb = cpt[bidx];
+        const int xb = pb % g.nx, yb = (pb / g.nx) % g.ny, zb = pb / (g.nx * g.ny);
+        const int64_t axs = R.A.x1 - R.A.x0, ays = R.A.y1 - R.A.y0;
+        const int64_t bxs = R.B.x1 - R.B.x0, bys = R.B.y1 - R.B.y0;
+        const int64_t al = ((int64_t)(za - R.A.z0) * ays + (ya - R.A.y0)) * axs + (xa - R.A.x0);
+        const int64_t bl = ((int64_t)(zb - R.B.z0) * bys + (yb - R.B.y0)) * bxs + (xb - R.B.x0);
+        key = pack_key(best, (uint32_t)(al * R.nB + bl));
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+        key = other > key ? other : key;
+      }
+      if (lane == 0 && key != 0ULL) atomicMax(keys + r, key);
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -393,10 +704,87 @@ void box_shape(int rows, int ax, int ay, int& bx, int& by, int& bz) {
 
 }  // namespace
 
+cudaError_t launch_pearson_block2(const corr_field* fa, const corr_field* fb, const RegionDev* hreg, int64_t nreg,
+                                  int absval, unsigned long long* keys, cudaStream_t st) {
+  int maxax = 1, maxay = 1, maxbx = 1, maxby = 1;
+  for (int64_t r = 0; r < nreg; ++r) {
+    const RegionDev& R = hreg[r];
+    maxax = std::max(maxax, R.A.x1 - R.A.x0);
+    maxay = std::max(maxay, R.A.y1 - R.A.y0);
+    maxbx = std::max(maxbx, R.B.x1 - R.B.x0);
+    maxby = std::max(maxby, R.B.y1 - R.B.y0);
+  }
+  GemmGeom g;
+  memset(&g, 0, sizeof(g));
+  box_shape(128, maxax, maxay, g.bxA, g.byA, g.bzA);
+  box_shape(128, maxbx, maxby, g.bxB, g.byB, g.bzB);
+  if (g.bzA > 256 || g.bzB > 256) return cudaErrorNotSupported;
+  g.nx = fa->nx;
+  g.ny = fa->ny;
+  g.kblocks = (fa->n_pad + BK - 1) / BK;
+  g.absval = absval;
+  g.same_field = fa == fb;
+  g.nreg = nreg;
+  std::vector<Gemm2Region> gr((size_t)nreg);
+  int64_t tiles = 0;
+  for (int64_t r = 0; r < nreg; ++r) {
+    const RegionDev& R = hreg[r];
+    Gemm2Region& G = gr[(size_t)r];
+    memset(&G, 0, sizeof(G));
+    G.A = R.A;
+    G.B = R.B;
+    G.ntA[0] = (R.A.x1 - R.A.x0 + g.bxA - 1) / g.bxA;
+    G.ntA[1] = (R.A.y1 - R.A.y0 + g.byA - 1) / g.byA;
+    G.ntA[2] = (R.A.z1 - R.A.z0 + g.bzA - 1) / g.bzA;
+    G.ntB[0] = (R.B.x1 - R.B.x0 + g.bxB - 1) / g.bxB;
+    G.ntB[1] = (R.B.y1 - R.B.y0 + g.byB - 1) / g.byB;
+    G.ntB[2] = (R.B.z1 - R.B.z0 + g.bzB - 1) / g.bzB;
+    G.nta = (int64_t)G.ntA[0] * G.ntA[1] * G.ntA[2];
+    G.ntb = (int64_t)G.ntB[0] * G.ntB[1] * G.ntB[2];
+    G.tile_off = tiles;
+    G.nA = R.nA;
+    G.nB = R.nB;
+    G.overlap = g.same_field && R.A.x0 < R.B.x1 && R.B.x0 < R.A.x1 && R.A.y0 < R.B.y1 && R.B.y0 < R.A.y1 &&
+                R.A.z0 < R.B.z1 && R.B.z0 < R.A.z1;
+    tiles += ((G.nta + 1) / 2) * ((G.ntb + 1) / 2);
+  }
+  g.total_tiles = tiles;
+  CUtensorMap mAhi, mAlo, mBhi, mBlo;
+  if (!make_map(&mAhi, fa->Zhi, fa, g.bxA, g.byA, g.bzA) || !make_map(&mAlo, fa->Zlo, fa, g.bxA, g.byA, g.bzA) ||
+      !make_map(&mBhi, fb->Zhi, fb, g.bxB, g.byB, g.bzB) || !make_map(&mBlo, fb->Zlo, fb, g.bxB, g.byB, g.bzB))
+    return cudaErrorNotSupported;
+  Gemm2Region* dgr = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&dgr, gr.size() * sizeof(Gemm2Region), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(dgr, gr.data(), gr.size() * sizeof(Gemm2Region), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  const size_t smem = 1024 + (size_t)STAGES2 * STAGE2_BYTES + 8 * (2 * STAGES2 + 4) + 16 + 2 * BN * 4 + 2 * BN * 4;
+  e = cudaFuncSetAttribute(pearson_block2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = kSMs;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t clusters = tiles < sms / 2 ? tiles : sms / 2;
+  pearson_block2_kernel<<<(unsigned)(2 * clusters), kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag,
+                                                                         fb->cflag, keys);
+  note_launch();
+  e = cudaGetLastError();
+  cudaFreeAsync(dgr, st);
+  return e;
+}
+
 cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, const RegionDev* hreg,
                                  const RegionDev* /*dreg*/, int64_t nreg, int absval, unsigned long long* keys,
                                  cudaStream_t st) {
   if (nreg == 0) return cudaSuccess;
+  static const int two_sm = [] {
+    const char* e = getenv("CORR_GEMM_2SM");  // opt-in: measured slower than the 1-SM kernel
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  if (two_sm) {
+    const cudaError_t e2 = launch_pearson_block2(fa, fb, hreg, nreg, absval, keys, st);
+    if (e2 != cudaErrorNotSupported) return e2;
+  }
   int maxax = 1, maxay = 1, maxbx = 1, maxby = 1;
   for (int64_t r = 0; r < nreg; ++r) {
     const RegionDev& R = hreg[r];
