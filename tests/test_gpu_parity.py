@@ -291,6 +291,26 @@ def test_pearson_block_n1000_and_two_fields():
     _block_compare(fa, None, ha, None, (sa.nx, sa.ny, sa.nz), A, B)
 
 
+def test_invariances_on_gpu_path():
+    """the oracle's bit-exact invariances re-run on the GPU path -- swap of
+    the two series (Eq. 1 symmetry), a common power-of-two scale, reflection of one field."""
+    spec = synth.field_spec(40, 30, 10, 1000, seed=77)
+    vals = synth.generate(spec, device="cuda")
+    f = cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members)
+    f4 = cb.corr_field_create((vals * 4.0).contiguous(), spec.nx, spec.ny, spec.nz, spec.members)
+    fneg = cb.corr_field_create((-vals).contiguous(), spec.nx, spec.ny, spec.nz, spec.members)
+    a, b = synth.random_pairs(spec.points, 500, seed=3)
+    a, b = a.cuda(), b.cuda()
+    for measure in (cb.CORR_KSG, cb.CORR_KSG | cb.CORR_F_KSG_PLUS1, cb.CORR_PEARSON):
+        base = cb.corr_eval_pairs(f, None, measure, 3, a, b)
+        assert torch.equal(base, cb.corr_eval_pairs(f, None, measure, 3, b, a))       # swap
+        assert torch.equal(base, cb.corr_eval_pairs(f4, None, measure, 3, a, b))      # 2^2 scale
+        refl = cb.corr_eval_pairs(fneg, f, measure, 3, a, b)                          # x -> -x
+        assert torch.equal(base, -refl if measure == cb.CORR_PEARSON else refl)
+    for g in (f, f4, fneg):
+        g.close()
+
+
 def test_dense_and_sweep_identical():
     """The exact sweep (default) and CORR_F_KSG_DENSE give bit-identical results."""
     spec = synth.spec_of(synth.C4)
