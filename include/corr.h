@@ -75,6 +75,15 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
 int corr_field_aggregate(const corr_field* f, int32_t fx, int32_t fy, int32_t fz, void* cuda_stream,
                          corr_field** out);
 
+/* corr_field_update -- replace the member values of an existing field (same dims and members;
+ * e.g. the next forecast time of the ensemble) and rebuild every derived buffer in place, with no
+ * device allocation.  values: float32 [members][nz][ny][nx], host or device.
+ * Work is ordered on `cuda_stream`, which is synchronised (validation); calls on other streams that
+ * still read the field must be ordered before it by the caller (events).  Errors: CORR_E_INVAL
+ * (non-finite value; the field content is then undefined until the next successful update),
+ * CORR_E_NOMEM (host input staging), CORR_E_CUDA. */
+int corr_field_update(corr_field* f, const float* values, void* cuda_stream);
+
 /* Frees the field's device memory (device-synchronising).  NULL is a no-op. */
 int corr_field_destroy(corr_field* f);
 

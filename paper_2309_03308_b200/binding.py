@@ -23,7 +23,7 @@ CORR_F_ABS = 1 << 9
 CORR_F_KSG_DENSE = 1 << 10
 CORR_OK, CORR_E_INVAL, CORR_E_RANGE, CORR_E_NOMEM, CORR_E_CUDA = 0, -1, -2, -3, -4
 
-EXPORTS = ("corr_field_create", "corr_field_aggregate", "corr_field_destroy", "corr_field_info", "corr_eval_pairs",
+EXPORTS = ("corr_field_create", "corr_field_update", "corr_field_aggregate", "corr_field_destroy", "corr_field_info", "corr_eval_pairs",
            "corr_region_max", "corr_ksg_debug", "corr_check", "corr_ksg_comparisons", "corr_launch_count",
            "corr_last_error")
 
@@ -57,6 +57,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     L.corr_field_create.argtypes = [vp, i32, i32, i32, i32, i32, vp, ctypes.POINTER(vp)]
     L.corr_field_destroy.argtypes = [vp]
     L.corr_field_aggregate.argtypes = [vp, i32, i32, i32, vp, ctypes.POINTER(vp)]
+    L.corr_field_update.argtypes = [vp, vp, vp]
     L.corr_field_info.argtypes = [vp] + [ctypes.POINTER(i32)] * 5
     L.corr_eval_pairs.argtypes = [vp, vp, i32, i32, vp, vp, i64, vp, vp]
     L.corr_region_max.argtypes = [vp, vp, i32, i32, ctypes.POINTER(corr_box), ctypes.POINTER(corr_box), i64,
@@ -133,6 +134,17 @@ def corr_field_create(values, nx: int, ny: int, nz: int, members: int, device: O
     _check(L.corr_field_create(ctypes.c_void_p(_ptr(values)), nx, ny, nz, members, device,
                                ctypes.c_void_p(st), ctypes.byref(h)))
     return Field(h.value, nx, ny, nz, members, device)
+
+
+def corr_field_update(field: Field, values, stream=None) -> Field:
+    """Re-ingest new member values (same shape) into `field` in place (no device allocation)."""
+    if isinstance(values, torch.Tensor):
+        assert values.dtype == torch.float32 and values.is_contiguous()
+        assert values.numel() == field.members * field.points
+    with torch.cuda.device(field.device):
+        st = _stream(stream)
+    _check(load().corr_field_update(ctypes.c_void_p(field.handle), ctypes.c_void_p(_ptr(values)), ctypes.c_void_p(st)))
+    return field
 
 
 def corr_field_aggregate(field: Field, fx: int, fy: int, fz: int, stream=None) -> Field:

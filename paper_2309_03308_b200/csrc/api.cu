@@ -99,13 +99,13 @@ int alloc_field(int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t dev
       !alloc((void**)&f->Zhi, row_elems * 4) || !alloc((void**)&f->Zlo, row_elems * 4) ||
       !alloc((void**)&f->S, row_elems * 4) || !alloc((void**)&f->perm, row_elems * 2) ||
       !alloc((void**)&f->cflag, (size_t)f->P) || !alloc((void**)&f->spread, (size_t)f->P * 4) ||
-      !alloc((void**)&f->psi, ((size_t)members + 2) * 8) || !alloc((void**)&f->err, sizeof(int))) {
+      !alloc((void**)&f->psi, ((size_t)members + 2) * 8) || !alloc((void**)&f->err, 2 * sizeof(int))) {
     free_field(f);
     return fail(CORR_E_NOMEM, "device allocation failed for the field");
   }
   const std::vector<double> psi = digamma_table(members);
   cudaError_t e = cudaMemcpyAsync(f->psi, psi.data(), psi.size() * 8, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(f->err, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(f->err, 0, 2 * sizeof(int), st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // psi is a stack vector
   if (e != cudaSuccess) {
     free_field(f);
@@ -117,6 +117,43 @@ int alloc_field(int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t dev
 
 int ksg_flags(int32_t measure) {
   return ((measure & CORR_F_KSG_PLUS1) ? 1 : 0) | ((measure & CORR_F_KSG_DENSE) ? 2 : 0);
+}
+
+// Copies member-major values (host or device) into f and rebuilds every derived buffer on `st`;
+// synchronises `st` (input validation).  The non-finite flag lives in err[1], the index-range
+// flag of corr_check in err[0].
+int ingest_values(corr_field* f, const float* values, cudaStream_t st, const char* who) {
+  auto alloc = [&](void** p, size_t bytes) -> bool {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  };
+  const float* dvalues = values;
+  float* staging = nullptr;
+  cudaPointerAttributes attr;
+  memset(&attr, 0, sizeof(attr));
+  const cudaError_t pe = cudaPointerGetAttributes(&attr, values);
+  if (pe != cudaSuccess) cudaGetLastError();
+  const bool on_device = pe == cudaSuccess &&
+                         (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
+                         attr.device == f->device;
+  cudaError_t e = cudaMemsetAsync(f->err + 1, 0, sizeof(int), st);
+  if (e == cudaSuccess && !on_device) {
+    const size_t bytes = (size_t)f->n * (size_t)f->P * 4;
+    if (!alloc((void**)&staging, bytes)) return fail(CORR_E_NOMEM, "device allocation failed for the input staging buffer");
+    e = cudaMemcpyAsync(staging, values, bytes, cudaMemcpyHostToDevice, st);
+    dvalues = staging;
+  }
+  if (e == cudaSuccess) e = launch_field_ingest(f, dvalues, st);
+  int herr = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, f->err + 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (staging) cudaFree(staging);
+  if (e != cudaSuccess) return cuda_fail(e, who);
+  if (herr & 2) return fail(CORR_E_INVAL, "non-finite input value (SPEC.md:72)");
+  return CORR_OK;
 }
 
 int check_pair_fields(const corr_field* fa, const corr_field*& fb) {
@@ -185,49 +222,21 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
   corr_field* f = nullptr;
   const int arc = alloc_field(nx, ny, nz, members, device, st, &f);
   if (arc) return arc;
-  cudaError_t e = cudaSuccess;
-  auto alloc = [&](void** p, size_t bytes) -> bool {
-    if (cudaMalloc(p, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    return true;
-  };
-
-  // values: device pointer on `device` -> used in place; otherwise staged through HBM
-  const float* dvalues = values;
-  float* staging = nullptr;
-  cudaPointerAttributes attr;
-  memset(&attr, 0, sizeof(attr));
-  cudaError_t pe = cudaPointerGetAttributes(&attr, values);
-  if (pe != cudaSuccess) cudaGetLastError();
-  const bool on_device = pe == cudaSuccess &&
-                         (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
-                         attr.device == device;
-  if (e == cudaSuccess && !on_device) {
-    const size_t bytes = (size_t)members * (size_t)f->P * 4;
-    if (!alloc((void**)&staging, bytes)) {
-      free_field(f);
-      return fail(CORR_E_NOMEM, "device allocation failed for the input staging buffer");
-    }
-    e = cudaMemcpyAsync(staging, values, bytes, cudaMemcpyHostToDevice, st);
-    dvalues = staging;
-  }
-  if (e == cudaSuccess) e = launch_field_ingest(f, dvalues, st);
-  int herr = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, f->err, sizeof(int), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (staging) cudaFree(staging);
-  if (e != cudaSuccess) {
+  const int rc = ingest_values(f, values, st, "corr_field_create");
+  if (rc) {
     free_field(f);
-    return cuda_fail(e, "corr_field_create");
-  }
-  if (herr & 2) {
-    free_field(f);
-    return fail(CORR_E_INVAL, "non-finite input value (SPEC.md:72)");
+    return rc;
   }
   *out = f;
   return CORR_OK;
+}
+
+int corr_field_update(corr_field* f, const float* values, void* cuda_stream) {
+  if (!f) return fail(CORR_E_INVAL, "field is NULL");
+  if (!values) return fail(CORR_E_INVAL, "values is NULL");
+  DeviceGuard guard(f->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  return ingest_values(f, values, (cudaStream_t)cuda_stream, "corr_field_update");
 }
 
 int corr_field_aggregate(const corr_field* f, int32_t fx, int32_t fy, int32_t fz, void* cuda_stream,

@@ -23,7 +23,7 @@ struct corr_field {
   uint8_t* cflag; // [P] 1 = constant series (min == max)
   float* spread;  // [P] ||x - mean|| (picks the sort marginal of a KSG pair)
   double* psi;    // [n + 2] digamma at integers, psi[0] = NaN
-  int* err;       // device status word: bit0 = index out of range, bit1 = non-finite input
+  int* err;       // device status words: err[0] bit0 = index out of range, err[1] bit1 = non-finite input
   void* tmaps;    // lazily built TMA descriptors (pearson_gemm.cu)
 };
 

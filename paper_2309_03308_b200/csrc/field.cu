@@ -194,7 +194,7 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
   const int64_t P = f->P;
   if (din) {
     dim3 grid((unsigned)((P + 31) / 32), (unsigned)((f->n_pad + 31) / 32));
-    transpose_kernel<<<grid, 256, 0, st>>>(din, f->F, f->n, f->n_pad, P, f->err);
+    transpose_kernel<<<grid, 256, 0, st>>>(din, f->F, f->n, f->n_pad, P, f->err + 1);
     note_launch();
   }
   {

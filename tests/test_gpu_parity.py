@@ -291,6 +291,35 @@ def test_pearson_block_n1000_and_two_fields():
     _block_compare(fa, None, ha, None, (sa.nx, sa.ny, sa.nz), A, B)
 
 
+def test_field_update_equals_fresh_create():
+    """corr_field_update (next ensemble, same shape, no reallocation) gives bit-identical results to
+    a field created from the same values; host and device inputs; non-finite input rejected."""
+    s1 = synth.field_spec(24, 16, 8, 100, seed=5)
+    s2 = synth.field_spec(24, 16, 8, 100, seed=6)
+    v1, v2 = synth.generate(s1, device="cuda"), synth.generate(s2, device="cuda")
+    f = cb.corr_field_create(v1, s1.nx, s1.ny, s1.nz, s1.members)
+    g = cb.corr_field_create(v2, s2.nx, s2.ny, s2.nz, s2.members)
+    a, b = synth.random_pairs(s1.points, 300, seed=4)
+    a, b = a.cuda(), b.cuda()
+    for src in (v2, v2.cpu().pin_memory(), v2.cpu()):
+        cb.corr_field_update(f, src)
+        for measure in (cb.CORR_KSG, cb.CORR_PEARSON):
+            assert torch.equal(cb.corr_eval_pairs(f, None, measure, 3, a, b),
+                               cb.corr_eval_pairs(g, None, measure, 3, a, b))
+        bricks = synth.partition(s1.nx, s1.ny, s1.nz, 8, 8, 4)
+        A, B = synth.context_pairs(bricks)
+        m1, a1 = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, A, B, 0, 0)
+        m2, a2 = cb.corr_region_max(g, None, cb.CORR_PEARSON, 0, A, B, 0, 0)
+        assert torch.equal(m1, m2) and torch.equal(a1, a2)
+    bad = v1.clone()
+    bad[1, 2] = float("inf")
+    with pytest.raises(cb.CorrError) as e:
+        cb.corr_field_update(f, bad)
+    assert e.value.code == cb.CORR_E_INVAL
+    cb.corr_field_update(f, v1)
+    cb.corr_check(f)
+
+
 def test_invariances_on_gpu_path():
     """the oracle's bit-exact invariances re-run on the GPU path -- swap of
     the two series (Eq. 1 symmetry), a common power-of-two scale, reflection of one field."""
