@@ -53,7 +53,7 @@ enum { CORR_OK = 0, CORR_E_INVAL = -1, CORR_E_RANGE = -2, CORR_E_NOMEM = -3, COR
 /* corr_field_create -- ingest one variable of an ensemble.
  *   values   : float32 [members][nz][ny][nx] (the paper's/SPEC's file order),
  *              host or device pointer (detected); copied, caller keeps ownership.
- *   nx,ny,nz : grid dims >= 1;  members (n) >= 2.
+ *   nx,ny,nz : grid dims >= 1;  2 <= members (n) <= 4096 (a pair is staged in shared memory).
  *   device   : CUDA ordinal the field lives on; the call makes it current.
  * Builds, on `device`: member-contiguous rows F[P][n_pad] (n_pad = ceil(n/8)*8),
  * fp64-standardised rows Z, their tf32 split (Z_hi, Z_lo), per-row sorted copies and

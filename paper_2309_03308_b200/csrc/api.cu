@@ -210,7 +210,7 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
   if (!values) return fail(CORR_E_INVAL, "values is NULL");
   if (nx < 1 || ny < 1 || nz < 1) return fail(CORR_E_INVAL, "grid dims must be >= 1");
   if (members < 2) return fail(CORR_E_INVAL, "members must be >= 2 (SPEC.md:34)");
-  if (members > 8192) return fail(CORR_E_INVAL, "members > 8192 not supported");
+  if (members > 4096) return fail(CORR_E_INVAL, "members > 4096 not supported (one pair is staged in shared memory)");
   int ndev = 0;
   const cudaError_t ce = cudaGetDeviceCount(&ndev);
   if (ce != cudaSuccess || ndev == 0) return cuda_fail(ce == cudaSuccess ? cudaErrorNoDevice : ce, "corr_field_create");

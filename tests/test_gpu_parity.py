@@ -291,6 +291,46 @@ def test_pearson_block_n1000_and_two_fields():
     _block_compare(fa, None, ha, None, (sa.nx, sa.ny, sa.nz), A, B)
 
 
+@pytest.mark.parametrize("n,k,npairs", [(2500, 3, 12), (2500, 32, 8), (4096, 5, 3), (20, 19, 60), (40, 32, 60)])
+def test_large_n_and_extreme_k(n, k, npairs):
+    """Member counts beyond one CTA pass (n up to the 4096 limit) and k = n-1 / k = 32 (the largest
+    register list)."""
+    spec = synth.field_spec(4, 4, 2, n, seed=n + k)
+    vals, f = _field(spec)
+    a, b = synth.random_pairs(spec.points, npairs, seed=k)
+    a, b = a.numpy(), b.numpy()
+    _check_knn(f, vals, k, a, b)
+    got = _cpu(cb.corr_eval_pairs(f, None, cb.CORR_KSG, k, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()))
+    ref = oracle.eval_pairs(vals.cpu(), None, oracle.KSG, k, a, b)
+    assert np.max(np.abs(got - ref)) <= KSG_TOL
+
+
+def test_degenerate_boxes_and_limits():
+    spec = synth.spec_of(synth.C1)
+    vals, f = _field(spec)
+    one = (3, 3, 1, 4, 4, 2)
+    m, arg = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, [one], [one], 0, 0)  # only the self pair
+    assert math.isnan(float(m[0])) and arg[0].tolist() == [-1, -1]
+    m, arg = cb.corr_region_max(f, None, cb.CORR_KSG, 3, [one], [one], 5, 0)
+    assert math.isnan(float(m[0])) and arg[0].tolist() == [-1, -1]
+    two = (0, 0, 0, 1, 1, 1)
+    for measure in (cb.CORR_KSG, cb.CORR_PEARSON):
+        m, arg = cb.corr_region_max(f, None, measure, 3, [two], [one], 1, 9)  # a single sample
+        ref, rarg = oracle.region_max(vals.cpu(), None, (8, 8, 4), measure, 3, [two], [one], 1, 9)
+        assert abs(float(m[0]) - ref[0]) <= KSG_TOL and arg[0].tolist() == list(rarg[0])
+    z, o = torch.zeros(1, dtype=torch.int64, device="cuda"), torch.ones(1, dtype=torch.int64, device="cuda")
+    v9 = cb.corr_eval_pairs(f, None, cb.CORR_KSG, 9, z, o)  # k = n - 1 is the largest valid k
+    assert abs(float(v9[0]) - oracle.eval_pairs(vals.cpu(), None, oracle.KSG, 9, [0], [1])[0]) <= KSG_TOL
+    with pytest.raises(cb.CorrError):
+        cb.corr_eval_pairs(f, None, cb.CORR_KSG, 10, z, o)
+    big = synth.field_spec(350, 200, 1, 4, seed=1)  # 70 000 points
+    bv, bf = _field(big)
+    full = (0, 0, 0, 350, 200, 1)
+    with pytest.raises(cb.CorrError) as e:
+        cb.corr_region_max(bf, None, cb.CORR_PEARSON, 0, [full], [full], 0, 0)  # |A||B| >= 2^32
+    assert e.value.code == cb.CORR_E_INVAL
+
+
 def test_field_update_equals_fresh_create():
     """corr_field_update (next ensemble, same shape, no reallocation) gives bit-identical results to
     a field created from the same values; host and device inputs; non-finite input rejected."""
