@@ -148,6 +148,19 @@ struct OwnBlock<K, RM, -1> {
   __device__ __forceinline__ static void run(const float4*, int, int, const float2 (&)[RM], float (&)[RM][K], int) {}
 };
 
+// one unfiltered 32-j chunk (no self pair inside): exact merge network on every value.  Used for
+// the chunks adjacent to the own block, where the filter would trigger on most groups anyway.
+template <int K, int RM>
+__device__ __forceinline__ void chunk_plain(const float4* __restrict__ cp, const float2 (&zi)[RM], float (&l)[RM][K]) {
+#pragma unroll 4
+  for (int h = 0; h < 16; ++h) {
+    const float4 v = cp[h];
+    const float2 z0 = make_float2(v.x, v.y), z1 = make_float2(v.z, v.w);
+#pragma unroll
+    for (int rr = 0; rr < RM; ++rr) merge2<K>(l[rr], cheb(zi[rr], z0), cheb(zi[rr], z1));
+  }
+}
+
 // one filtered 32-j chunk, groups of G j's (G = 4 or 8) per vote
 template <int K, int RM, int G, bool DESC>
 __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
@@ -183,6 +196,8 @@ __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, co
     }
   }
 }
+
+constexpr bool PLAIN_NEAR = true;
 
 template <int K, int RM, int G, bool SWEEP>
 __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sorted_kernel(
@@ -310,7 +325,8 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
           if (!need) {
             hlo = -1;
           } else {
-            chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l);
+            if (PLAIN_NEAR && hlo == c0 - 1) chunk_plain<K, RM>(xy4 + hlo * 16, zi, l);
+            else chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l);
             --hlo;
             ++nproc;
           }
@@ -327,7 +343,8 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
           if (!need) {
             hhi = nh;
           } else {
-            chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l);
+            if (PLAIN_NEAR && hhi == c1) chunk_plain<K, RM>(xy4 + hhi * 16, zi, l);
+            else chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l);
             ++hhi;
             ++nproc;
           }
