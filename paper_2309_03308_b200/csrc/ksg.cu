@@ -79,23 +79,48 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
 // Power-of-two steps over an array padded with +inf to 2^LOG2 > n entries (the padding
 // satisfies both predicates): pos = number of leading "not P" elements; every probe is an LDS
 // with an immediate offset, the step sequence is uniform across the warp.
-template <int ST>
-__device__ __forceinline__ int marginal_count(const float* __restrict__ S, int log2p, float v, float e) {
-  if (!(e > 0.f)) return 0;
-  const uint32_t base = (uint32_t)__cvta_generic_to_shared(S);
-  uint32_t au = base, aw = base;
-#pragma unroll
-  for (int b = 13; b >= 0; --b) {
-    if (b < log2p) {
-      constexpr uint32_t kStride = ST * 4;
-      const uint32_t step = (1u << b) * kStride;
-      const float su = lds_f32(au + step - kStride);
-      const float sw = lds_f32(aw + step - kStride);
-      au = (su - v >= e) ? au : au + step;   // not yet P_u -> move right
-      aw = (v - sw < e) ? aw : aw + step;    // not yet P_w -> move right
+template <int OFF>
+__device__ __forceinline__ float lds_imm(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
+  return v;
+}
+
+// The four searches of one member (u and w on the sorted marginal x -- stride 8 B inside xy --
+// and on the sorted y row), interleaved; step 2^B is a compile-time immediate offset.
+template <int B>
+struct CountSearch {
+  __device__ __forceinline__ static void run(int log2p, uint32_t& xu, uint32_t& xw, uint32_t& yu, uint32_t& yw,
+                                             float x, float y, float e) {
+    if (B < log2p) {
+      constexpr int SX = (1 << B) * 8, SY = (1 << B) * 4;
+      const float pxu = lds_imm<SX - 8>(xu), pxw = lds_imm<SX - 8>(xw);
+      const float pyu = lds_imm<SY - 4>(yu), pyw = lds_imm<SY - 4>(yw);
+      xu = (pxu - x >= e) ? xu : xu + SX;  // not yet P_u -> move right
+      xw = (x - pxw < e) ? xw : xw + SX;   // not yet P_w -> move right
+      yu = (pyu - y >= e) ? yu : yu + SY;
+      yw = (y - pyw < e) ? yw : yw + SY;
     }
+    CountSearch<B - 1>::run(log2p, xu, xw, yu, yw, x, y, e);
   }
-  return (int)((au - aw) / (ST * 4)) - 1;
+};
+template <>
+struct CountSearch<-1> {
+  __device__ __forceinline__ static void run(int, uint32_t&, uint32_t&, uint32_t&, uint32_t&, float, float, float) {}
+};
+
+// Strict marginal counts of a member (x, y) with radius e: returns n_x, n_y.
+__device__ __forceinline__ void marginal_counts(const float2* __restrict__ xy, const float* __restrict__ sy,
+                                                int log2p, float x, float y, float e, int& cx, int& cy) {
+  if (!(e > 0.f)) {
+    cx = cy = 0;
+    return;
+  }
+  const uint32_t bx = (uint32_t)__cvta_generic_to_shared(xy), by = (uint32_t)__cvta_generic_to_shared(sy);
+  uint32_t xu = bx, xw = bx, yu = by, yw = by;
+  CountSearch<12>::run(log2p, xu, xw, yu, yw, x, y, e);
+  cx = (int)((xu - xw) >> 3) - 1;
+  cy = (int)((yu - yw) >> 2) - 1;
 }
 
 // own-block chunk: exact network; the self pair j == i exists only for member RC of each lane
@@ -361,8 +386,8 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
             for (int t = 0; t < K - 1; ++t)
               if (t == k - 1) e = l[rr][t];
           }
-          const int cu = marginal_count<2>(reinterpret_cast<const float*>(xy), log2p, zi[rr].x, e);
-          const int cv = marginal_count<1>(sy, log2p, zi[rr].y, e);
+          int cu, cv;
+          marginal_counts(xy, sy, log2p, zi[rr].x, zi[rr].y, e, cu, cv);
           acc += psi[cu + off] + psi[cv + off];
           if (out.dbg_eps) {
             const int m = pm[ts[rr]];
