@@ -70,15 +70,6 @@ __device__ __forceinline__ void merge2(float (&l)[K], float d0, float d1) {
 //           are monotone in s by monotone rounding, and imply / cover s >= v because e > 0);
 //           [w, u) holds every s with |fl(s - v)| < e, the member itself included -> u - w - 1.
 // Branch-free lower bounds (uniform trip count), the two searches interleaved for ILP.
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
-}
-
-// Power-of-two steps over an array padded with +inf to 2^LOG2 > n entries (the padding
-// satisfies both predicates): pos = number of leading "not P" elements; every probe is an LDS
-// with an immediate offset, the step sequence is uniform across the warp.
 template <int OFF>
 __device__ __forceinline__ float lds_imm(uint32_t addr) {
   float v;
@@ -222,8 +213,6 @@ __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, co
   }
 }
 
-constexpr bool PLAIN_NEAR = true;
-
 template <int K, int RM, int G, bool SWEEP>
 __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
@@ -350,7 +339,7 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
           if (!need) {
             hlo = -1;
           } else {
-            if (PLAIN_NEAR && hlo == c0 - 1) chunk_plain<K, RM>(xy4 + hlo * 16, zi, l);
+            if (hlo == c0 - 1) chunk_plain<K, RM>(xy4 + hlo * 16, zi, l);
             else chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l);
             --hlo;
             ++nproc;
@@ -368,7 +357,7 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sort
           if (!need) {
             hhi = nh;
           } else {
-            if (PLAIN_NEAR && hhi == c1) chunk_plain<K, RM>(xy4 + hhi * 16, zi, l);
+            if (hhi == c1) chunk_plain<K, RM>(xy4 + hhi * 16, zi, l);
             else chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l);
             ++hhi;
             ++nproc;
@@ -448,31 +437,13 @@ cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus
   return cudaGetLastError();
 }
 
-int env_int(const char* name, int dflt) {
-  const char* s = getenv(name);
-  return s && *s ? atoi(s) : dflt;
-}
-
 template <int K>
 cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                      const PairOut& out, cudaStream_t st) {
-  // CORR_KSG_SWEEP=0 disables the exact sweep (dense n(n-1) comparisons); CORR_KSG_RM picks
-  // members per lane (1, 2 or 4) and CORR_KSG_G the filter group (4, or 8 with RM = 1).
-  // plus1 bit 1 = CORR_F_KSG_DENSE: disable the exact sweep for this call
-  static const int sweep_env = env_int("CORR_KSG_SWEEP", 1);
-  const int sweep = sweep_env && !(plus1 & 2);
-  static const int rm = env_int("CORR_KSG_RM", 1);
-  static const int g = env_int("CORR_KSG_G", 4);
-#define CORR_KSG_CASE(RMv, Gv)                                                 \
-  if (rm == RMv && g == Gv)                                                   \
-    return sweep ? launch_t<K, RMv, Gv, true>(fa, fb, k, plus1, src, out, st) \
-                 : launch_t<K, RMv, Gv, false>(fa, fb, k, plus1, src, out, st);
-  CORR_KSG_CASE(1, 8)
-  CORR_KSG_CASE(2, 4)
-  CORR_KSG_CASE(4, 4)
-#undef CORR_KSG_CASE
-  return sweep ? launch_t<K, 1, 4, true>(fa, fb, k, plus1, src, out, st)
-               : launch_t<K, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  // Default: the exact sweep with one member per lane (RM = 1).  CORR_F_KSG_DENSE (plus1 bit 1)
+  // evaluates all n(n-1) comparisons with the 4-members-per-lane layout (the faster dense form).
+  if (plus1 & 2) return launch_t<K, 4, 4, false>(fa, fb, k, plus1, src, out, st);
+  return launch_t<K, 1, 4, true>(fa, fb, k, plus1, src, out, st);
 }
 
 }  // namespace
@@ -494,7 +465,7 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int pl
   // NEXT #2 (paper default k = ceil(3n/100)): register lists of 12/16/24/32;
   // inserting d >= l[KT-1] >= l[k-1] cannot change the k smallest, so the filter and the sweep
   // stay exact with the longer list, and eps = l[k-1].
-  const bool sweep = env_int("CORR_KSG_SWEEP", 1) != 0 && !(plus1 & 2);
+  const bool sweep = !(plus1 & 2);
   if (k <= 12) return sweep ? launch_t<12, 1, 4, true>(fa, fb, k, plus1, src, out, st)
                             : launch_t<12, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   if (k <= 16) return sweep ? launch_t<16, 1, 4, true>(fa, fb, k, plus1, src, out, st)
