@@ -13,6 +13,8 @@
 // All kernels are HBM-bound; DESIGN.md lists their algorithmic bytes.
 #include <math.h>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "corr_internal.cuh"
 
 namespace corr {
@@ -149,6 +151,59 @@ __global__ void __launch_bounds__(512) sort_kernel(const float* __restrict__ F, 
   }
 }
 
+// ---- 3b. per-row radix sort (one CTA of T threads x I items per row, N2 = T*I) ------
+// The bitonic network above costs log2(N2)(log2(N2)+1)/2 shared-memory passes with a
+// barrier each (55 at n = 1000); an LSD radix sort of order-preserving u32 keys needs 8
+// 4-bit passes.  Keys: u = bits(f); u ^= (u >> 31 ? 0xFFFFFFFF : 0x80000000) (finite
+// inputs, checked at ingest), so u32 order == float order (-0 before +0; equal floats
+// compare equal in every consumer, and KSG only needs SOME sorted permutation, R4).
+// Values: the member index.  Rows are loaded striped (coalesced) and written striped.
+template <int T, int I>
+__global__ void __launch_bounds__(T) sort_radix_kernel(const float* __restrict__ F, float* __restrict__ S,
+                                                       uint16_t* __restrict__ perm, int n, int n_pad, int64_t P) {
+  using Sorter = cub::BlockRadixSort<uint32_t, T, I, uint16_t>;
+  __shared__ typename Sorter::TempStorage tmp;
+  for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
+    const float* row = F + p * n_pad;
+    uint32_t key[I];
+    uint16_t idx[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const int e = i * T + (int)threadIdx.x;
+      uint32_t u = 0xFFFFFFFFu;  // +inf pad sorts last (its key is below 0xFFFFFFFF: never equal)
+      if (e < n) {
+        u = __float_as_uint(row[e]);
+        u ^= (u >> 31) ? 0xFFFFFFFFu : 0x80000000u;
+      }
+      key[i] = u;
+      idx[i] = (uint16_t)(e < n ? e : 0xFFFF);
+    }
+    Sorter(tmp).SortBlockedToStriped(key, idx);
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const int e = i * T + (int)threadIdx.x;
+      if (e < n_pad) {
+        uint32_t u = key[i];
+        u ^= (u >> 31) ? 0x80000000u : 0xFFFFFFFFu;
+        S[p * n_pad + e] = e < n ? __uint_as_float(u) : INFINITY;
+        perm[p * n_pad + e] = e < n ? idx[i] : (uint16_t)0xFFFF;
+      }
+    }
+    __syncthreads();  // tmp is reused by the next row
+  }
+}
+
+template <int T, int I>
+cudaError_t launch_sort_radix(corr_field* f, cudaStream_t st) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sort_radix_kernel<T, I>, T, 0);
+  if (occ < 1) occ = 1;
+  int64_t blocks = (int64_t)kSMs * occ * 8;
+  if (blocks > f->P) blocks = f->P;
+  sort_radix_kernel<T, I><<<(unsigned)blocks, T, 0, st>>>(f->F, f->S, f->perm, f->n, f->n_pad, f->P);
+  return cudaSuccess;
+}
+
 // ---- 4. mean-tree level (§3.3): per-member block means ----------
 // One warp per coarse point; lanes stride over members, so every fine row is read with
 // coalesced loads and the coarse row is written contiguously.  fp64 sums, fp32 means; a
@@ -206,6 +261,21 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
     int log2n2 = 1;
     while ((1 << log2n2) < f->n) ++log2n2;
     const int N2 = 1 << log2n2;
+    cudaError_t er = cudaErrorInvalidValue;
+    switch (N2) {
+      case 64: er = launch_sort_radix<32, 2>(f, st); break;
+      case 128: er = launch_sort_radix<32, 4>(f, st); break;
+      case 256: er = launch_sort_radix<64, 4>(f, st); break;
+      case 512: er = launch_sort_radix<64, 8>(f, st); break;
+      case 1024: er = launch_sort_radix<128, 8>(f, st); break;
+      case 2048: er = launch_sort_radix<256, 8>(f, st); break;
+      case 4096: er = launch_sort_radix<256, 16>(f, st); break;
+      default: break;
+    }
+    if (er == cudaSuccess) {
+      note_launch(2);
+      return cudaGetLastError();
+    }
     const int tpr = N2 / 2 < 512 ? N2 / 2 : 512;
     int threads = 512;
     if (threads < tpr) threads = tpr;

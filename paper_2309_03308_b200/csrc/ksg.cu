@@ -182,7 +182,7 @@ template <int K, int RM, int G, bool DESC>
 __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
                                                float (&l)[RM][K]) {
   constexpr int NG = 32 / G;
-#pragma unroll 2
+#pragma unroll 4
   for (int gi = 0; gi < NG; ++gi) {
     const int g = DESC ? NG - 1 - gi : gi;
     float2 z[G];
@@ -214,7 +214,7 @@ __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, co
 }
 
 template <int K, int RM, int G, bool SWEEP>
-__global__ void __launch_bounds__(256, (K > 8 ? 2 : (RM == 1 ? 4 : 3))) ksg_sorted_kernel(
+__global__ void __launch_bounds__(128, (K > 8 ? 4 : (RM == 1 ? 8 : 6))) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
     const float* __restrict__ Sb, const uint16_t* __restrict__ Pb, const float* __restrict__ Fb,
     const float* __restrict__ spa, const float* __restrict__ spb, const uint8_t* __restrict__ ca,
@@ -421,7 +421,7 @@ cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus
                       (size_t)(nsy + n_pad) * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
                       34 * sizeof(double) + 8 * 64 * sizeof(float2);
   auto kern = ksg_sorted_kernel<K, RM, G, SWEEP>;
-  const int warps = nblk < 8 ? nblk : 8;
+  const int warps = nblk < 4 ? nblk : 4;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int occ = 0;

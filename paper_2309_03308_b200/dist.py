@@ -60,6 +60,31 @@ def gather_region_results(out_max: torch.Tensor, out_arg: torch.Tensor, bounds: 
     return full_max, full_arg
 
 
+def member_bounds(members: int, world: int) -> List[Tuple[int, int]]:
+    """Contiguous member-row slices [lo, hi) of a [members][points] field, one per rank."""
+    return [(members * r // world, members * (r + 1) // world) for r in range(world)]
+
+
+def replicate_field_sharded(host_slice: torch.Tensor, out: torch.Tensor, rank: int, world: int, group=None,
+                            stream=None) -> int:
+    """Builds a full field replica on every rank from 1/world of it per rank.
+
+    Rank r copies ITS member rows (``host_slice``, pinned host memory, rows
+    member_bounds()[r]) into ``out[lo:hi]`` over its own PCIe link, then every rank
+    broadcasts its slice to the others (NVLink/NVSwitch under NCCL).  Each GPU thus
+    receives 1/world of the field from the host instead of rank 0 uploading all of it.
+    Returns the host->device bytes this rank copied."""
+    bounds = member_bounds(out.shape[0], world)
+    lo, hi = bounds[rank]
+    if hi > lo:
+        out[lo:hi].copy_(host_slice, non_blocking=True)
+    if world > 1:
+        for r, (a, b) in enumerate(bounds):
+            if b > a:
+                tdist.broadcast(out[a:b], r, group=group)
+    return (hi - lo) * out.shape[1] * out.element_size()
+
+
 def split_box_z(box, world: int):
     """Split one region box into `world` slabs along its longest axis (focus view, one
     region pair: SURVEY.md §8(e) "C2 ... split A into R row slabs")."""

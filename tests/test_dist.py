@@ -82,3 +82,35 @@ def test_gloo_shards_gather_bit_identical(world):
         assert np.array_equal(fm, m.astype(np.float32))  # every rank holds the full result
         assert np.array_equal(fa, a)
         assert v == fm_ref[0] and tuple(ab) == tuple(fa_ref[0])
+
+
+def _repl_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    spec = synth.spec_of(synth.C1)
+    full = synth.generate(spec)                      # [members][points]; every rank knows only its slice
+    lo, hi = cdist.member_bounds(spec.members, world)[rank]
+    out = torch.full_like(full, float("nan"))
+    nbytes = cdist.replicate_field_sharded(full[lo:hi].clone(), out, rank, world)
+    q.put((rank, bool(torch.equal(out, full)), nbytes))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_field_replication(world):
+    """Each rank uploads 1/world of the member rows; the broadcasts rebuild the full replica
+    bit for bit on every rank (bench.py e2e at N > 1)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_repl_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spec = synth.spec_of(synth.C1)
+    assert all(ok for _, ok, _ in res)
+    assert sum(b for _, _, b in res) == spec.members * spec.points * 4
