@@ -213,6 +213,49 @@ __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, co
   }
 }
 
+// ---- a2 staging through the TMA unit: 1-D bulk copies global -> shared with an mbarrier
+// (cp.async.bulk, contiguous rows: no tensor map needed) and bulk L2 prefetches of the
+// next pair's rows, so a CTA's next staging finds its rows in L2.
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(b)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Side-effect-free peek at unit u's point pair (prefetch only; errors are raised when the
+// unit itself is processed).
+__device__ __forceinline__ bool peek_pair(const PairSrc& s, int64_t u, int64_t& a, int64_t& b) {
+  if (s.mode == kList) {
+    a = s.idxA[u];
+    b = s.idxB[u];
+    return a >= 0 && a < s.P && b >= 0 && b < s.P;
+  }
+  int64_t r;
+  uint32_t idx;
+  return unit_pair(s, u, a, b, r, idx);
+}
+
 template <int K, int RM, int G, bool SWEEP>
 __global__ void __launch_bounds__(128, (K > 8 ? 4 : (RM == 1 ? 8 : 6))) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
@@ -241,10 +284,15 @@ __global__ void __launch_bounds__(128, (K > 8 ? 4 : (RM == 1 ? 8 : 6))) ksg_sort
   uint16_t* pm = reinterpret_cast<uint16_t*>(tb + n_pad);
   double* red = reinterpret_cast<double*>(pm + n_pad + 8);
   int* next_blk = reinterpret_cast<int*>(red + 32);
+  uint64_t* stage_bar = reinterpret_cast<uint64_t*>(red + 33);
   float2* dupbuf = reinterpret_cast<float2*>(red + 34);  // [8 warps][64] (RM == 1 own chunk)
 
   for (int i = threadIdx.x; i < n + 2; i += nthreads) psi[i] = psi_g[i];
+  for (int t = n_pad + threadIdx.x; t < nsy; t += nthreads) sy[t] = INFINITY;  // never overwritten
+  if (threadIdx.x == 0) bar_init(stage_bar);
   __syncthreads();
+  uint32_t stage_phase = 0;
+  const uint32_t row_bytes = (uint32_t)n_pad * 4u;
   const double psi_nk = psi[n] + psi[k];
   const int off = plus1 ? 1 : 0;
   unsigned long long executed = 0;
@@ -268,16 +316,27 @@ __global__ void __launch_bounds__(128, (K > 8 ? 4 : (RM == 1 ? 8 : 6))) ksg_sort
     const uint16_t* Pu = swap ? Pb + b * n_pad : Pa + a * n_pad;
     const float* Fv = swap ? Fa + a * n_pad : Fb + b * n_pad;
     const float* Sv = swap ? Sa + a * n_pad : Sb + b * n_pad;
-    __syncthreads();
-    if (threadIdx.x == 0) *next_blk = nwarps;  // blocks 0..nwarps-1 are taken statically
-    // ---- a2: stage ----
-    for (int q = threadIdx.x; q < n_pad / 4; q += nthreads) {
-      reinterpret_cast<float4*>(tb)[q] = __ldg(reinterpret_cast<const float4*>(Fv) + q);
-      reinterpret_cast<float4*>(sy)[q] = __ldg(reinterpret_cast<const float4*>(Sv) + q);
-      reinterpret_cast<uint2*>(pm)[q] = __ldg(reinterpret_cast<const uint2*>(Pu) + q);
+    __syncthreads();  // the previous pair is done with sy, tb, pm
+    // ---- a2: stage (bulk copies by one thread; L2 prefetch of this CTA's next pair) ----
+    if (threadIdx.x == 0) {
+      *next_blk = nwarps;  // blocks 0..nwarps-1 are taken statically
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_expect(stage_bar, 2u * row_bytes + row_bytes / 2u);
+      bulk_g2s(tb, Fv, row_bytes, stage_bar);
+      bulk_g2s(sy, Sv, row_bytes, stage_bar);
+      bulk_g2s(pm, Pu, row_bytes / 2u, stage_bar);
+      int64_t a2, b2;
+      if (u + gridDim.x < src.nunits && peek_pair(src, u + gridDim.x, a2, b2)) {
+        bulk_prefetch_l2(Sa + a2 * n_pad, row_bytes);
+        bulk_prefetch_l2(Fa + a2 * n_pad, row_bytes);
+        bulk_prefetch_l2(Pa + a2 * n_pad, row_bytes / 2u);
+        bulk_prefetch_l2(Sb + b2 * n_pad, row_bytes);
+        bulk_prefetch_l2(Fb + b2 * n_pad, row_bytes);
+        bulk_prefetch_l2(Pb + b2 * n_pad, row_bytes / 2u);
+      }
     }
-    for (int t = n_pad + threadIdx.x; t < nsy; t += nthreads) sy[t] = INFINITY;
-    __syncthreads();
+    bar_wait(stage_bar, stage_phase);
+    stage_phase ^= 1u;
     for (int q = threadIdx.x; q < nxy / 4; q += nthreads) {
       const int t = 4 * q;
       float4 xs = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
