@@ -166,9 +166,10 @@ struct OwnBlock<K, RM, -1> {
 
 // one unfiltered 32-j chunk (no self pair inside): exact merge network on every value.  Used for
 // the chunks adjacent to the own block, where the filter would trigger on most groups anyway.
+// Fully unrolled so every shared load is issued well ahead of its FADD2.
 template <int K, int RM>
 __device__ __forceinline__ void chunk_plain(const float4* __restrict__ cp, const float2 (&zi)[RM], float (&l)[RM][K]) {
-#pragma unroll 4
+#pragma unroll(RM == 1 ? 16 : 4)
   for (int h = 0; h < 16; ++h) {
     const float4 v = cp[h];
     const float2 z0 = make_float2(v.x, v.y), z1 = make_float2(v.z, v.w);
@@ -177,12 +178,13 @@ __device__ __forceinline__ void chunk_plain(const float4* __restrict__ cp, const
   }
 }
 
-// one filtered 32-j chunk, groups of G j's (G = 4 or 8) per vote
+// one filtered 32-j chunk, groups of G j's per vote (RM > 1: the dense 4-members-per-lane
+// layout, compact loop)
 template <int K, int RM, int G, bool DESC>
-__device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
-                                               float (&l)[RM][K]) {
+__device__ __forceinline__ void chunk_filtered_rm(const float4* __restrict__ cp, const float2 (&zi)[RM],
+                                                  float (&l)[RM][K]) {
   constexpr int NG = 32 / G;
-#pragma unroll 4
+#pragma unroll 2
   for (int gi = 0; gi < NG; ++gi) {
     const int g = DESC ? NG - 1 - gi : gi;
     float2 z[G];
@@ -209,6 +211,58 @@ __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, co
 #pragma unroll
         for (int q = 0; q < G; q += 2) merge2<K>(l[rr], d[rr][q], d[rr][q + 1]);
       }
+    }
+  }
+}
+
+// one filtered 32-j chunk, groups of G j's per vote; the next group's shared loads are issued
+// before this group's vote (software pipelining across the data-dependent branch)
+template <int K, int RM, int G, bool DESC>
+__device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
+                                               float (&l)[RM][K]) {
+  if constexpr (RM > 1) {
+    chunk_filtered_rm<K, RM, G, DESC>(cp, zi, l);
+    return;
+  }
+  constexpr int NG = 32 / G, NQ = G / 2;
+  float4 cur[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) cur[q] = cp[(DESC ? NG - 1 : 0) * NQ + q];
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    const int g = DESC ? NG - 1 - gi : gi;
+    float4 nxt[NQ];
+    if (gi + 1 < NG) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) nxt[q] = cp[(DESC ? g - 1 : g + 1) * NQ + q];
+    }
+    float2 z[G];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      z[2 * q] = make_float2(cur[q].x, cur[q].y);
+      z[2 * q + 1] = make_float2(cur[q].z, cur[q].w);
+    }
+    float d[RM][G];
+    bool p = false;
+#pragma unroll
+    for (int rr = 0; rr < RM; ++rr) {
+#pragma unroll
+      for (int q = 0; q < G; ++q) d[rr][q] = cheb(zi[rr], z[q]);
+      float m = d[rr][0];
+#pragma unroll
+      for (int q = 1; q < G; ++q) m = fminf(m, d[rr][q]);
+      p |= m < l[rr][K - 1];
+    }
+    if (__any_sync(0xffffffffu, p)) {
+#pragma unroll
+      for (int rr = 0; rr < RM; ++rr) {
+#pragma unroll
+        for (int q = 0; q < G; q += 2) merge2<K>(l[rr], d[rr][q], d[rr][q + 1]);
+      }
+    }
+    if (gi + 1 < NG) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
     }
   }
 }
@@ -257,7 +311,7 @@ __device__ __forceinline__ bool peek_pair(const PairSrc& s, int64_t u, int64_t& 
 }
 
 template <int K, int RM, int G, bool SWEEP>
-__global__ void __launch_bounds__(128, (K > 8 ? 4 : (RM == 1 ? 8 : 6))) ksg_sorted_kernel(
+__global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? 8 : 3))) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
     const float* __restrict__ Sb, const uint16_t* __restrict__ Pb, const float* __restrict__ Fb,
     const float* __restrict__ spa, const float* __restrict__ spb, const uint8_t* __restrict__ ca,
@@ -276,24 +330,24 @@ __global__ void __launch_bounds__(128, (K > 8 ? 4 : (RM == 1 ? 8 : 6))) ksg_sort
   const int nsy = max(n_pad, 1 << log2p);
   const int nch = (n + 31) >> 5;
 
-  double* psi = reinterpret_cast<double*>(smem_raw);
-  const int psi_len = (n + 2 + 1) & ~1;
-  float2* xy = reinterpret_cast<float2*>(smem_raw + psi_len * sizeof(double));
+  // psi(m) is read through L1 from the field's fp64 table (8 KB at n = 1000, shared by all
+  // CTAs of an SM): keeping it out of shared memory lets 8 CTAs fit per SM
+  const double* __restrict__ psi = psi_g;
+  float2* xy = reinterpret_cast<float2*>(smem_raw);
   float* sy = reinterpret_cast<float*>(xy + nxy);
   float* tb = sy + nsy;
   uint16_t* pm = reinterpret_cast<uint16_t*>(tb + n_pad);
   double* red = reinterpret_cast<double*>(pm + n_pad + 8);
   int* next_blk = reinterpret_cast<int*>(red + 32);
   uint64_t* stage_bar = reinterpret_cast<uint64_t*>(red + 33);
-  float2* dupbuf = reinterpret_cast<float2*>(red + 34);  // [8 warps][64] (RM == 1 own chunk)
+  float2* dupbuf = reinterpret_cast<float2*>(red + 34);  // [warps][64] (RM == 1 own chunk)
 
-  for (int i = threadIdx.x; i < n + 2; i += nthreads) psi[i] = psi_g[i];
   for (int t = n_pad + threadIdx.x; t < nsy; t += nthreads) sy[t] = INFINITY;  // never overwritten
   if (threadIdx.x == 0) bar_init(stage_bar);
   __syncthreads();
   uint32_t stage_phase = 0;
   const uint32_t row_bytes = (uint32_t)n_pad * 4u;
-  const double psi_nk = psi[n] + psi[k];
+  const double psi_nk = __ldg(psi + n) + __ldg(psi + k);
   const int off = plus1 ? 1 : 0;
   unsigned long long executed = 0;
 
@@ -327,12 +381,11 @@ __global__ void __launch_bounds__(128, (K > 8 ? 4 : (RM == 1 ? 8 : 6))) ksg_sort
       bulk_g2s(pm, Pu, row_bytes / 2u, stage_bar);
       int64_t a2, b2;
       if (u + gridDim.x < src.nunits && peek_pair(src, u + gridDim.x, a2, b2)) {
-        bulk_prefetch_l2(Sa + a2 * n_pad, row_bytes);
-        bulk_prefetch_l2(Fa + a2 * n_pad, row_bytes);
-        bulk_prefetch_l2(Pa + a2 * n_pad, row_bytes / 2u);
-        bulk_prefetch_l2(Sb + b2 * n_pad, row_bytes);
-        bulk_prefetch_l2(Fb + b2 * n_pad, row_bytes);
-        bulk_prefetch_l2(Pb + b2 * n_pad, row_bytes / 2u);
+        const bool swap2 = spb[b2] > spa[a2];  // the four rows that pair will stage
+        bulk_prefetch_l2(swap2 ? Sb + b2 * n_pad : Sa + a2 * n_pad, row_bytes);
+        bulk_prefetch_l2(swap2 ? Pb + b2 * n_pad : Pa + a2 * n_pad, row_bytes / 2u);
+        bulk_prefetch_l2(swap2 ? Fa + a2 * n_pad : Fb + b2 * n_pad, row_bytes);
+        bulk_prefetch_l2(swap2 ? Sa + a2 * n_pad : Sb + b2 * n_pad, row_bytes);
       }
     }
     bar_wait(stage_bar, stage_phase);
@@ -436,7 +489,7 @@ __global__ void __launch_bounds__(128, (K > 8 ? 4 : (RM == 1 ? 8 : 6))) ksg_sort
           }
           int cu, cv;
           marginal_counts(xy, sy, log2p, zi[rr].x, zi[rr].y, e, cu, cv);
-          acc += psi[cu + off] + psi[cv + off];
+          acc += __ldg(psi + cu + off) + __ldg(psi + cv + off);
           if (out.dbg_eps) {
             const int m = pm[ts[rr]];
             out.dbg_eps[u * n + m] = e;
@@ -476,11 +529,11 @@ cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus
   const int nxy = std::max(((n + 127) / 128) * 128, 1 << log2p);
   const int nsy = std::max(n_pad, 1 << log2p);
   const int nblk = (n + 32 * RM - 1) / (32 * RM);
-  const size_t smem = (size_t)((n + 2 + 1) & ~1) * sizeof(double) + (size_t)nxy * sizeof(float2) +
-                      (size_t)(nsy + n_pad) * sizeof(float) + ((size_t)n_pad + 8) * sizeof(uint16_t) +
-                      34 * sizeof(double) + 8 * 64 * sizeof(float2);
+  const int wmax = RM == 1 ? 4 : 8;  // 4-warp CTAs (8/SM) for the sweep; 8-warp CTAs for the dense layout
+  const int warps = nblk < wmax ? nblk : wmax;
+  const size_t smem = (size_t)nxy * sizeof(float2) + (size_t)(nsy + n_pad) * sizeof(float) +
+                      ((size_t)n_pad + 8) * sizeof(uint16_t) + 34 * sizeof(double) + (size_t)warps * 64 * sizeof(float2);
   auto kern = ksg_sorted_kernel<K, RM, G, SWEEP>;
-  const int warps = nblk < 4 ? nblk : 4;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int occ = 0;
