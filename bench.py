@@ -113,8 +113,8 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- workload
-def workload(samples: int):
-    cfg = synth.C4
+def workload(samples: int, name: str = "c4"):
+    cfg = {"c4": synth.C4, "c3": synth.C3}[name]
     spec = synth.spec_of(cfg)
     A, B = synth.context_pairs(synth.bricks_of(cfg))
     return cfg, spec, A, B
@@ -146,22 +146,22 @@ def oracle_sample_run(spec, A, B, samples, npairs, seed):
     mini = synth.rows(spec, torch.tensor(pts)).T.contiguous().numpy()
     ia = np.array([pos[a] for a, _ in pairs], np.int64)
     ib = np.array([pos[b] for _, b in pairs], np.int64)
-    oracle.lib()
+    threads = oracle.set_threads(cpu_count())  # torchrun exports OMP_NUM_THREADS=1
     t = time.perf_counter()
     vals = oracle.eval_pairs(mini, None, oracle.KSG, K_NN, ia, ib)
     dt = time.perf_counter() - t
-    return npairs / dt, dt, vals
+    return npairs / dt, dt, vals, threads
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg, spec, A, B = workload(args.samples)
-    cores = cpu_count()
     npairs = args.ref_pairs
     times = []
+    cores = None
     for i in range(args.warmup + args.steps):
-        _, dt, _ = oracle_sample_run(spec, A, B, args.samples, npairs, SEED + i)
+        _, dt, _, cores = oracle_sample_run(spec, A, B, args.samples, npairs, SEED + i)
         if i >= args.warmup:
             times.append(dt)
     ms = 1e3 * float(np.mean(times))
@@ -178,9 +178,10 @@ def run_reference(args, rank, world):
 
 
 def config_dict(cfg, args, world):
-    return {"workload": f"C4 context view: 250x352x20 grid, n=1000 members, 88 bricks 32x32x20, 3828 region "
-                        f"pairs x S={args.samples} sampled point pairs, KSG k=3 region max (+ Pearson sampled "
-                        f"region max + Pearson exhaustive focus block)",
+    name = "C4" if cfg.members == 1000 else "C3 (dry run only; not the BASELINE config)"
+    return {"workload": f"{name} context view: {cfg.nx}x{cfg.ny}x{cfg.nz} grid, n={cfg.members} members, 88 bricks "
+                        f"32x32x20, 3828 region pairs x S={args.samples} sampled point pairs, KSG k=3 region max "
+                        f"(+ Pearson sampled region max + Pearson exhaustive focus block)",
             "grid": [cfg.nx, cfg.ny, cfg.nz], "members": cfg.members, "k": K_NN, "region_pairs": 3828,
             "samples_per_region_pair": args.samples, "parallelism": f"region-pair shards x{world}",
             "l2": "inputs larger than L2 (field rows 7 GB x planes, random rows per pair)"}
@@ -204,6 +205,8 @@ def main():
     ap.add_argument("--cpu-pairs", type=int, default=768)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c3"],
+                    help="c4 = the BASELINE metric's config (default); c3 (n=100) only for dry runs")
     args = ap.parse_args()
 
     rank = env_int("RANK", 0)
@@ -213,10 +216,18 @@ def main():
         run_reference(args, rank, world)
         return
 
+    local = local % torch.cuda.device_count()  # identity on a node with one GPU per rank
     torch.cuda.set_device(local)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg, spec, A, B = workload(args.samples)
+        # BENCH_DIST_BACKEND=gloo: host-side collectives, for dry-running the multi-rank
+        # orchestration with several ranks on ONE GPU (no rank waits inside a kernel); numbers
+        # taken that way are not scaling results
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
+    cfg, spec, A, B = workload(args.samples, args.workload)
     R = len(A)
     S = args.samples
     bounds = cdist.shard_bounds([S] * R, world)
@@ -263,7 +274,7 @@ def main():
             pm, pa = cdist.gather_region_results(pm, pa, bounds)
             fparts = [torch.empty((1, 3), dtype=torch.int64, device=fm.device) for _ in range(world)]
             packed = torch.cat([fm.view(torch.int32).to(torch.int64).view(1, 1), fa.view(1, 2)], 1)
-            tdist.all_gather(fparts, packed)
+            cdist.all_gather(fparts, packed)
             fm = torch.stack([p[0, 0].to(torch.int32).view(torch.float32) for p in fparts])
             fa = torch.stack([p[0, 1:] for p in fparts])
         return km, ka, pm, pa, fm, fa
@@ -435,8 +446,8 @@ def main():
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, _ = oracle_sample_run(spec, A, B, S, args.cpu_pairs, SEED)
-        cpu_base = {"value": v, "unit": UNIT, "cores": cpu_count(), "kind": "oracle",
+        v, dt, _, threads = oracle_sample_run(spec, A, B, S, args.cpu_pairs, SEED)
+        cpu_base = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                     "sample": f"first {args.cpu_pairs} sampled pairs of the C4 context view (n=1000, k=3), "
                               f"oracle.eval_pairs, {dt:.1f} s"}
 

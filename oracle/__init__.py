@@ -73,8 +73,15 @@ def lib():
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(Box), ctypes.POINTER(Box), ctypes.c_int64,
                                         ctypes.c_int64, ctypes.c_uint64, F64P, I64P]
+        L.oracle_set_threads.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads for the oracle's pair loops (n <= 0: query only); returns the count used."""
+    return int(lib().oracle_set_threads(int(n)))
 
 
 # measure codes (same values as include/corr.h, restated: the oracle shares no header)

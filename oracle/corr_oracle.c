@@ -27,6 +27,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <omp.h>
+
 #define ORACLE_NAN ((double)NAN)
 
 /* ------------------------------------------------------------------------- */
@@ -308,4 +310,13 @@ void oracle_region_max(const float* fa, const float* fb, int nx, int ny, int nz,
     out_argmax[2 * r] = ba;
     out_argmax[2 * r + 1] = bb;
   }
+}
+
+/* Host threads used by the OpenMP loops above (not arithmetic: every pair is computed by one
+ * thread, so results do not depend on it).  n <= 0 leaves the setting alone.  Returns the
+ * thread count the next parallel region will use.  bench.py sets it explicitly because
+ * torchrun exports OMP_NUM_THREADS=1. */
+int oracle_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
 }

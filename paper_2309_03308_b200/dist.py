@@ -38,6 +38,18 @@ def shard_bounds(weights: Sequence[int], world: int) -> List[Tuple[int, int]]:
     return bounds
 
 
+def all_gather(parts: List[torch.Tensor], t: torch.Tensor, group=None) -> None:
+    """all_gather that also runs under gloo with CUDA tensors (staged through host memory),
+    so the multi-rank orchestration can be dry-run on one GPU; NCCL gathers in place."""
+    if t.is_cuda and tdist.get_backend(group) == "gloo":
+        host = [torch.empty(p.shape, dtype=p.dtype) for p in parts]
+        tdist.all_gather(host, t.cpu(), group=group)
+        for p, h in zip(parts, host):
+            p.copy_(h)
+        return
+    tdist.all_gather(parts, t, group=group)
+
+
 def gather_region_results(out_max: torch.Tensor, out_arg: torch.Tensor, bounds: Sequence[Tuple[int, int]],
                           group=None) -> Tuple[torch.Tensor, torch.Tensor]:
     """All-gather the shards' (max, argmax) into the full [R] / [R, 2] result on every rank.
@@ -52,7 +64,7 @@ def gather_region_results(out_max: torch.Tensor, out_arg: torch.Tensor, bounds: 
     packed[:m, 0] = out_max.view(torch.int32).to(torch.int64)
     packed[:m, 1:] = out_arg
     parts = [torch.empty_like(packed) for _ in range(world)]
-    tdist.all_gather(parts, packed, group=group)
+    all_gather(parts, packed, group=group)
     rows = [parts[r][: hi - lo] for r, (lo, hi) in enumerate(bounds)]
     allrows = torch.cat(rows, 0)
     full_max = allrows[:, 0].to(torch.int32).view(torch.float32).clone()
@@ -65,8 +77,7 @@ def member_bounds(members: int, world: int) -> List[Tuple[int, int]]:
     return [(members * r // world, members * (r + 1) // world) for r in range(world)]
 
 
-def replicate_field_sharded(host_slice: torch.Tensor, out: torch.Tensor, rank: int, world: int, group=None,
-                            stream=None) -> int:
+def replicate_field_sharded(host_slice: torch.Tensor, out: torch.Tensor, rank: int, world: int, group=None) -> int:
     """Builds a full field replica on every rank from 1/world of it per rank.
 
     Rank r copies ITS member rows (``host_slice``, pinned host memory, rows
