@@ -310,6 +310,109 @@ __device__ __forceinline__ bool peek_pair(const PairSrc& s, int64_t u, int64_t& 
   return unit_pair(s, u, a, b, r, idx);
 }
 
+// ---- a3 / a4 / a5 for one member block (32*RM sort-consecutive members) of a staged pair:
+// own block, outward chunks with the exact sweep, marginal counts, psi sum into acc.
+// xy: interleaved (x, y) in x order (+inf pad to nxy), sy: sorted y (+inf pad to nsy),
+// dup: this warp's 64-entry scratch (RM == 1), pm: the x argsort (debug dump only).
+template <int K, int RM, int G, bool SWEEP>
+__device__ __forceinline__ void ksg_block(const float2* __restrict__ xy, const float* __restrict__ sy,
+                                          float2* __restrict__ dup, int n, int nch, int log2p, int mb, int lane,
+                                          int k, const double* __restrict__ psi, int off, double& acc,
+                                          unsigned long long& executed, const PairOut& out, int64_t u,
+                                          const uint16_t* __restrict__ pm, bool swap) {
+  constexpr int BLK = 32 * RM;
+  const float4* xy4 = reinterpret_cast<const float4*>(xy);
+  float2 zi[RM];
+  float l[RM][K];
+  int ts[RM];
+#pragma unroll
+  for (int rr = 0; rr < RM; ++rr) {
+    ts[rr] = mb * BLK + 32 * rr + lane;
+    zi[rr] = xy[ts[rr]];
+#pragma unroll
+    for (int t = 0; t < K; ++t) l[rr][t] = INFINITY;
+  }
+  const int c0 = mb * RM;
+  const int c1 = min(c0 + RM, nch);
+  if constexpr (RM == 1) {
+    const float2 zc = xy[c0 * 32 + lane];
+    dup[lane] = zc;
+    dup[lane + 32] = zc;
+    __syncwarp();
+    own_rotated<K>(dup, lane, zi[0], l[0]);
+    __syncwarp();
+  } else {
+    OwnBlock<K, RM, RM - 1>::run(xy4, c0, nch, zi, l, lane);
+  }
+  // outward in chunks of 32 j; below descending, above ascending
+  const int nh = nch;
+  int nproc = c1 - c0;
+  int hlo = c0 - 1, hhi = c1;
+  while (hlo >= 0 || hhi < nh) {
+    // SWEEP: per-member exact test -- member i still needs the chunk iff the x-gap to the
+    // chunk's nearest edge is below its current k-th distance: fl(x_i - x_edge) < l_i[K-1]
+    // (below) or fl(x_edge - x_i) < l_i[K-1] (above).  Skip the direction once no lane does.
+    if (hlo >= 0) {
+      bool need = true;
+      if (SWEEP) {
+        const float xe = xy[hlo * 32 + 31].x;
+        bool p = false;
+#pragma unroll
+        for (int rr = 0; rr < RM; ++rr) p |= (ts[rr] < n) && (zi[rr].x - xe < l[rr][K - 1]);
+        need = __any_sync(0xffffffffu, p);
+      }
+      if (!need) {
+        hlo = -1;
+      } else {
+        if (hlo == c0 - 1) chunk_plain<K, RM>(xy4 + hlo * 16, zi, l);
+        else chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l);
+        --hlo;
+        ++nproc;
+      }
+    }
+    if (hhi < nh) {
+      bool need = true;
+      if (SWEEP) {
+        const float xe = xy[hhi * 32].x;
+        bool p = false;
+#pragma unroll
+        for (int rr = 0; rr < RM; ++rr) p |= (ts[rr] < n) && (xe - zi[rr].x < l[rr][K - 1]);
+        need = __any_sync(0xffffffffu, p);
+      }
+      if (!need) {
+        hhi = nh;
+      } else {
+        if (hhi == c1) chunk_plain<K, RM>(xy4 + hhi * 16, zi, l);
+        else chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l);
+        ++hhi;
+        ++nproc;
+      }
+    }
+  }
+  const int valid = min(BLK, n - mb * BLK);
+  if (lane == 0) executed += (unsigned long long)nproc * 32ull * (unsigned long long)valid;
+#pragma unroll
+  for (int rr = 0; rr < RM; ++rr) {
+    if (ts[rr] < n) {
+      float e = l[rr][K - 1];
+      if (K > 8) {  // list longer than k: eps = l[k-1] (the K smallest are exact)
+#pragma unroll
+        for (int t = 0; t < K - 1; ++t)
+          if (t == k - 1) e = l[rr][t];
+      }
+      int cu, cv;
+      marginal_counts(xy, sy, log2p, zi[rr].x, zi[rr].y, e, cu, cv);
+      acc += __ldg(psi + cu + off) + __ldg(psi + cv + off);
+      if (out.dbg_eps) {
+        const int m = pm[ts[rr]];
+        out.dbg_eps[u * n + m] = e;
+        out.dbg_nx[u * n + m] = swap ? cv : cu;
+        out.dbg_ny[u * n + m] = swap ? cu : cv;
+      }
+    }
+  }
+}
+
 template <int K, int RM, int G, bool SWEEP>
 __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? 8 : 3))) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
@@ -404,100 +507,11 @@ __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? 8
     __syncthreads();
 
     // ---- a3 / a4 / a5 ----
-    const float4* xy4 = reinterpret_cast<const float4*>(xy);
     double acc = 0.0;
     // member blocks: first one static, then dynamic (sweep lengths differ per block)
     for (int mb = warp; mb < nblk;) {
-      float2 zi[RM];
-      float l[RM][K];
-      int ts[RM];
-#pragma unroll
-      for (int rr = 0; rr < RM; ++rr) {
-        ts[rr] = mb * BLK + 32 * rr + lane;
-        zi[rr] = xy[ts[rr]];
-#pragma unroll
-        for (int t = 0; t < K; ++t) l[rr][t] = INFINITY;
-      }
-      const int c0 = mb * RM;
-      const int c1 = min(c0 + RM, nch);
-      if constexpr (RM == 1) {
-        float2* dup = dupbuf + warp * 64;
-        const float2 zc = xy[c0 * 32 + lane];
-        dup[lane] = zc;
-        dup[lane + 32] = zc;
-        __syncwarp();
-        own_rotated<K>(dup, lane, zi[0], l[0]);
-        __syncwarp();
-      } else {
-        OwnBlock<K, RM, RM - 1>::run(xy4, c0, nch, zi, l, lane);
-      }
-      // outward in chunks of 32 j; below descending, above ascending
-      const int nh = nch;
-      int nproc = c1 - c0;
-      int hlo = c0 - 1, hhi = c1;
-      while (hlo >= 0 || hhi < nh) {
-        // SWEEP: per-member exact test -- member i still needs the chunk iff the x-gap to the
-        // chunk's nearest edge is below its current k-th distance: fl(x_i - x_edge) < l_i[K-1]
-        // (below) or fl(x_edge - x_i) < l_i[K-1] (above).  Skip the direction once no lane does.
-        if (hlo >= 0) {
-          bool need = true;
-          if (SWEEP) {
-            const float xe = xy[hlo * 32 + 31].x;
-            bool p = false;
-#pragma unroll
-            for (int rr = 0; rr < RM; ++rr) p |= (ts[rr] < n) && (zi[rr].x - xe < l[rr][K - 1]);
-            need = __any_sync(0xffffffffu, p);
-          }
-          if (!need) {
-            hlo = -1;
-          } else {
-            if (hlo == c0 - 1) chunk_plain<K, RM>(xy4 + hlo * 16, zi, l);
-            else chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l);
-            --hlo;
-            ++nproc;
-          }
-        }
-        if (hhi < nh) {
-          bool need = true;
-          if (SWEEP) {
-            const float xe = xy[hhi * 32].x;
-            bool p = false;
-#pragma unroll
-            for (int rr = 0; rr < RM; ++rr) p |= (ts[rr] < n) && (xe - zi[rr].x < l[rr][K - 1]);
-            need = __any_sync(0xffffffffu, p);
-          }
-          if (!need) {
-            hhi = nh;
-          } else {
-            if (hhi == c1) chunk_plain<K, RM>(xy4 + hhi * 16, zi, l);
-            else chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l);
-            ++hhi;
-            ++nproc;
-          }
-        }
-      }
-      const int valid = min(BLK, n - mb * BLK);
-      if (lane == 0) executed += (unsigned long long)nproc * 32ull * (unsigned long long)valid;
-#pragma unroll
-      for (int rr = 0; rr < RM; ++rr) {
-        if (ts[rr] < n) {
-          float e = l[rr][K - 1];
-          if (K > 8) {  // list longer than k: eps = l[k-1] (the K smallest are exact)
-#pragma unroll
-            for (int t = 0; t < K - 1; ++t)
-              if (t == k - 1) e = l[rr][t];
-          }
-          int cu, cv;
-          marginal_counts(xy, sy, log2p, zi[rr].x, zi[rr].y, e, cu, cv);
-          acc += __ldg(psi + cu + off) + __ldg(psi + cv + off);
-          if (out.dbg_eps) {
-            const int m = pm[ts[rr]];
-            out.dbg_eps[u * n + m] = e;
-            out.dbg_nx[u * n + m] = swap ? cv : cu;
-            out.dbg_ny[u * n + m] = swap ? cu : cv;
-          }
-        }
-      }
+      ksg_block<K, RM, G, SWEEP>(xy, sy, dupbuf + warp * 64, n, nch, log2p, mb, lane, k, psi, off, acc, executed,
+                                 out, u, pm, swap);
       int nb = 0;
       if (lane == 0) nb = atomicAdd(next_blk, 1);
       mb = __shfl_sync(0xffffffffu, nb, 0);
@@ -549,11 +563,162 @@ cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus
   return cudaGetLastError();
 }
 
+
+// ---- small n (n < 128): one WARP per pair, no CTA barriers ------------------------------
+// At n = 100 (the paper's usual member count) a pair is only 4 member blocks; with a CTA per
+// pair the end-of-pair barrier and the staging latency dominate (ncu: 27 % barrier stalls).
+// Here each warp owns its pairs end to end: two staging slots per warp, the NEXT pair's four
+// rows are bulk-copied (cp.async.bulk, its own mbarrier) while the current pair is computed,
+// and the psi sum is reduced with shuffles.  Same per-block code (ksg_block) as the CTA kernel.
+constexpr int kWarpKernelMaxN = 127;  // 2^log2p <= 128: every per-warp array fits 4.8 KB
+
+struct WarpSlotMeta {
+  int64_t a, b, r;
+  uint32_t idx;
+  int flags;  // bit0 ok, bit1 degenerate, bit2 swap, bit3 rows staged
+};
+
+template <int K, bool SWEEP>
+__global__ void __launch_bounds__(128, 8) ksg_warp_kernel(
+    const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
+    const float* __restrict__ Sb, const uint16_t* __restrict__ Pb, const float* __restrict__ Fb,
+    const float* __restrict__ spa, const float* __restrict__ spb, const uint8_t* __restrict__ ca,
+    const uint8_t* __restrict__ cb, const double* __restrict__ psi, int n, int n_pad, int k, int plus1,
+    PairSrc src, PairOut out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  int log2p = 1;
+  while ((1 << log2p) <= n) ++log2p;
+  constexpr int NXY = 128, NSY = 128;  // 2^log2p <= 128 and n_pad <= 128
+  const int nblk = (n + 31) >> 5;
+  const int nch = nblk;
+  // per-warp layout: xy[128] float2 | dup[64] float2 | 2 slots x {sy[128], tb[n_pad], su[n_pad], pm[n_pad+8]}
+  //                  | meta[2] | bar[2]
+  const int slot_bytes = NSY * 4 + 2 * n_pad * 4 + (n_pad + 8) * 2;
+  const int warp_bytes = NXY * 8 + 64 * 8 + 2 * slot_bytes + 2 * (int)sizeof(WarpSlotMeta) + 16;
+  unsigned char* wb = smem_raw + warp * ((warp_bytes + 15) & ~15);
+  float2* xy = reinterpret_cast<float2*>(wb);
+  float2* dup = xy + NXY;
+  unsigned char* slots = reinterpret_cast<unsigned char*>(dup + 64);
+  WarpSlotMeta* meta = reinterpret_cast<WarpSlotMeta*>(slots + 2 * slot_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(meta + 2);
+  auto slot_sy = [&](int s) { return reinterpret_cast<float*>(slots + s * slot_bytes); };
+  auto slot_tb = [&](int s) { return slot_sy(s) + NSY; };
+  auto slot_su = [&](int s) { return slot_tb(s) + n_pad; };
+  auto slot_pm = [&](int s) { return reinterpret_cast<uint16_t*>(slot_su(s) + n_pad); };
+
+  for (int s = 0; s < 2; ++s)
+    for (int t = n_pad + lane; t < NSY; t += 32) slot_sy(s)[t] = INFINITY;  // never overwritten
+  if (lane == 0) {
+    bar_init(bars + 0);
+    bar_init(bars + 1);
+  }
+  __syncwarp();
+  const uint32_t row_bytes = (uint32_t)n_pad * 4u;
+  const double psi_nk = __ldg(psi + n) + __ldg(psi + k);
+  const int off = plus1 ? 1 : 0;
+  unsigned long long executed = 0;
+  const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t u0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+
+  // lane 0: resolve unit u into slot s and start its four row copies
+  auto issue = [&](int s, int64_t u) {
+    WarpSlotMeta m;
+    const bool ok = unit_pair(src, u, m.a, m.b, m.r, m.idx);
+    m.flags = ok ? 1 : 0;
+    if (ok) {
+      const bool degenerate = (ca[m.a] | cb[m.b]) != 0;
+      const bool swap = spb[m.b] > spa[m.a];
+      m.flags |= (degenerate ? 2 : 0) | (swap ? 4 : 0);
+      if (!degenerate || out.dbg_eps != nullptr) {
+        m.flags |= 8;
+        const float* Su = swap ? Sb + m.b * n_pad : Sa + m.a * n_pad;
+        const uint16_t* Pu = swap ? Pb + m.b * n_pad : Pa + m.a * n_pad;
+        const float* Fv = swap ? Fa + m.a * n_pad : Fb + m.b * n_pad;
+        const float* Sv = swap ? Sa + m.a * n_pad : Sb + m.b * n_pad;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bar_expect(bars + s, 3u * row_bytes + row_bytes / 2u);
+        bulk_g2s(slot_sy(s), Sv, row_bytes, bars + s);
+        bulk_g2s(slot_tb(s), Fv, row_bytes, bars + s);
+        bulk_g2s(slot_su(s), Su, row_bytes, bars + s);
+        bulk_g2s(slot_pm(s), Pu, row_bytes / 2u, bars + s);
+      }
+    }
+    meta[s] = m;
+  };
+
+  if (lane == 0 && u0 < src.nunits) issue(0, u0);
+  uint32_t phase = 0;  // bit s = parity of slot s's next completion
+  int it = 0;
+  for (int64_t u = u0; u < src.nunits; u += W, ++it) {
+    const int s = it & 1;
+    if (lane == 0 && u + W < src.nunits) issue(s ^ 1, u + W);
+    __syncwarp();
+    const WarpSlotMeta m = meta[s];
+    if (!(m.flags & 1) || !(m.flags & 8)) {  // invalid / self pair, or degenerate without debug dump
+      if (src.mode == kList && lane == 0) out.out[u] = NAN;
+      __syncwarp();
+      continue;
+    }
+    bar_wait(bars + s, (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const bool swap = (m.flags & 4) != 0;
+    const float* sy = slot_sy(s);
+    const float* tb = slot_tb(s);
+    const float* su = slot_su(s);
+    const uint16_t* pm = slot_pm(s);
+    for (int t = lane; t < NXY; t += 32)
+      xy[t] = t < n ? make_float2(su[t], tb[pm[t]]) : make_float2(INFINITY, INFINITY);
+    __syncwarp();
+    double acc = 0.0;
+    for (int mb = 0; mb < nblk; ++mb)
+      ksg_block<K, 1, 4, SWEEP>(xy, sy, dup, n, nch, log2p, mb, lane, k, psi, off, acc, executed, out, u, pm, swap);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const float mi = (m.flags & 2) ? NAN : (float)(psi_nk - acc / (double)n);
+      if (src.mode == kList) {
+        out.out[u] = mi;
+      } else if (!isnan(mi)) {
+        atomicMax(out.keys + m.r, pack_key(out.absval ? fabsf(mi) : mi, m.idx));
+      }
+    }
+    __syncwarp();  // slot s and xy are free: the next iteration's issue may overwrite slot s
+  }
+  if (lane == 0 && executed) atomicAdd(&g_ksg_comparisons, executed);
+}
+
+template <int K, bool SWEEP>
+cudaError_t launch_warp(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
+                        const PairOut& out, cudaStream_t st) {
+  const int n = fa->n, n_pad = fa->n_pad;
+  const int slot_bytes = 128 * 4 + 2 * n_pad * 4 + (n_pad + 8) * 2;
+  const int warp_bytes = (128 * 8 + 64 * 8 + 2 * slot_bytes + 2 * (int)sizeof(WarpSlotMeta) + 16 + 15) & ~15;
+  const size_t smem = (size_t)4 * warp_bytes;
+  auto kern = ksg_warp_kernel<K, SWEEP>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
+  if (occ < 1) occ = 1;
+  int64_t blocks = (src.nunits + 3) / 4;
+  const int64_t cap = (int64_t)kSMs * occ;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, 128, smem, st>>>(fa->S, fa->perm, fa->F, fb->S, fb->perm, fb->F, fa->spread, fb->spread,
+                                            fa->cflag, fb->cflag, fa->psi, n, n_pad, k, plus1 & 1, src, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
 template <int K>
 cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
                      const PairOut& out, cudaStream_t st) {
   // Default: the exact sweep with one member per lane (RM = 1).  CORR_F_KSG_DENSE (plus1 bit 1)
   // evaluates all n(n-1) comparisons with the 4-members-per-lane layout (the faster dense form).
+  if (fa->n <= kWarpKernelMaxN)
+    return (plus1 & 2) ? launch_warp<K, false>(fa, fb, k, plus1, src, out, st)
+                       : launch_warp<K, true>(fa, fb, k, plus1, src, out, st);
   if (plus1 & 2) return launch_t<K, 4, 4, false>(fa, fb, k, plus1, src, out, st);
   return launch_t<K, 1, 4, true>(fa, fb, k, plus1, src, out, st);
 }
