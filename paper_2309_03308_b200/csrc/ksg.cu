@@ -146,7 +146,7 @@ __device__ __forceinline__ void insert1(float (&l)[K], float d) {
 template <int K>
 __device__ __forceinline__ void own_rotated(const float2* __restrict__ dup, int lane, float2 zi, float (&l)[K]) {
   const float2* p = dup + lane;
-#pragma unroll
+#pragma unroll(K <= 8 ? 15 : 1)
   for (int s = 1; s < 31; s += 2) merge2<K>(l, cheb(zi, p[s]), cheb(zi, p[s + 1]));
   insert1<K>(l, cheb(zi, p[31]));
 }
@@ -169,7 +169,7 @@ struct OwnBlock<K, RM, -1> {
 // Fully unrolled so every shared load is issued well ahead of its FADD2.
 template <int K, int RM>
 __device__ __forceinline__ void chunk_plain(const float4* __restrict__ cp, const float2 (&zi)[RM], float (&l)[RM][K]) {
-#pragma unroll(RM == 1 ? 16 : 4)
+#pragma unroll((RM == 1 && K <= 8) ? 16 : 2)
   for (int h = 0; h < 16; ++h) {
     const float4 v = cp[h];
     const float2 z0 = make_float2(v.x, v.y), z1 = make_float2(v.z, v.w);
@@ -178,8 +178,8 @@ __device__ __forceinline__ void chunk_plain(const float4* __restrict__ cp, const
   }
 }
 
-// one filtered 32-j chunk, groups of G j's per vote (RM > 1: the dense 4-members-per-lane
-// layout, compact loop)
+// one filtered 32-j chunk, groups of G j's per vote, compact loop (RM > 1: the dense
+// 4-members-per-lane layout; K > 8: the long lists of the paper's k = ceil(3n/100))
 template <int K, int RM, int G, bool DESC>
 __device__ __forceinline__ void chunk_filtered_rm(const float4* __restrict__ cp, const float2 (&zi)[RM],
                                                   float (&l)[RM][K]) {
@@ -220,7 +220,7 @@ __device__ __forceinline__ void chunk_filtered_rm(const float4* __restrict__ cp,
 template <int K, int RM, int G, bool DESC>
 __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
                                                float (&l)[RM][K]) {
-  if constexpr (RM > 1) {
+  if constexpr (RM > 1 || K > 8) {  // compact loop: long lists make the unrolled body too big for the i-cache
     chunk_filtered_rm<K, RM, G, DESC>(cp, zi, l);
     return;
   }
