@@ -151,6 +151,17 @@ __device__ __forceinline__ void own_rotated(const float2* __restrict__ dup, int 
   insert1<K>(l, cheb(zi, p[31]));
 }
 
+// RM == 1 own block with only v < 32 members (the last block when 32 does not divide n): dup
+// holds the block with period v, so s = 1..v-1 visits the v-1 others (lanes >= v are padding).
+template <int K>
+__device__ __forceinline__ void own_rotated_part(const float2* __restrict__ dup, int lane, float2 zi, float (&l)[K],
+                                                 int v) {
+  const float2* p = dup + lane;
+  int s = 1;
+  for (; s + 1 < v; s += 2) merge2<K>(l, cheb(zi, p[s]), cheb(zi, p[s + 1]));
+  if (s < v) insert1<K>(l, cheb(zi, p[s]));
+}
+
 template <int K, int RM, int RC>
 struct OwnBlock {
   __device__ __forceinline__ static void run(const float4* xy4, int c0, int nch, const float2 (&zi)[RM],
@@ -168,7 +179,16 @@ struct OwnBlock<K, RM, -1> {
 // the chunks adjacent to the own block, where the filter would trigger on most groups anyway.
 // Fully unrolled so every shared load is issued well ahead of its FADD2.
 template <int K, int RM>
-__device__ __forceinline__ void chunk_plain(const float4* __restrict__ cp, const float2 (&zi)[RM], float (&l)[RM][K]) {
+__device__ __forceinline__ void chunk_plain(const float4* __restrict__ cp, const float2 (&zi)[RM], float (&l)[RM][K],
+                                            int cnt) {
+  if (cnt < 32) {  // the partial last chunk: compact loop over its (cnt + 1) / 2 float4s
+    for (int h = 0; h < ((cnt + 1) >> 1); ++h) {
+      const float4 v = cp[h];
+#pragma unroll
+      for (int rr = 0; rr < RM; ++rr) merge2<K>(l[rr], cheb(zi[rr], make_float2(v.x, v.y)), cheb(zi[rr], make_float2(v.z, v.w)));
+    }
+    return;
+  }
 #pragma unroll((RM == 1 && K <= 8) ? 16 : 2)
   for (int h = 0; h < 16; ++h) {
     const float4 v = cp[h];
@@ -182,10 +202,11 @@ __device__ __forceinline__ void chunk_plain(const float4* __restrict__ cp, const
 // 4-members-per-lane layout; K > 8: the long lists of the paper's k = ceil(3n/100))
 template <int K, int RM, int G, bool DESC>
 __device__ __forceinline__ void chunk_filtered_rm(const float4* __restrict__ cp, const float2 (&zi)[RM],
-                                                  float (&l)[RM][K]) {
+                                                  float (&l)[RM][K], int cnt) {
   constexpr int NG = 32 / G;
+  const int ng = (cnt + G - 1) / G;  // DESC chunks are always full (the partial chunk is the last)
 #pragma unroll 2
-  for (int gi = 0; gi < NG; ++gi) {
+  for (int gi = 0; gi < ng; ++gi) {
     const int g = DESC ? NG - 1 - gi : gi;
     float2 z[G];
 #pragma unroll
@@ -219,9 +240,13 @@ __device__ __forceinline__ void chunk_filtered_rm(const float4* __restrict__ cp,
 // before this group's vote (software pipelining across the data-dependent branch)
 template <int K, int RM, int G, bool DESC>
 __device__ __forceinline__ void chunk_filtered(const float4* __restrict__ cp, const float2 (&zi)[RM],
-                                               float (&l)[RM][K]) {
+                                               float (&l)[RM][K], int cnt) {
   if constexpr (RM > 1 || K > 8) {  // compact loop: long lists make the unrolled body too big for the i-cache
-    chunk_filtered_rm<K, RM, G, DESC>(cp, zi, l);
+    chunk_filtered_rm<K, RM, G, DESC>(cp, zi, l, cnt);
+    return;
+  }
+  if (!DESC && cnt < 32) {  // the partial last chunk (only ever scanned upward): compact loop
+    chunk_filtered_rm<K, RM, G, DESC>(cp, zi, l, cnt);
     return;
   }
   constexpr int NG = 32 / G, NQ = G / 2;
@@ -314,7 +339,10 @@ __device__ __forceinline__ bool peek_pair(const PairSrc& s, int64_t u, int64_t& 
 // own block, outward chunks with the exact sweep, marginal counts, psi sum into acc.
 // xy: interleaved (x, y) in x order (+inf pad to nxy), sy: sorted y (+inf pad to nsy),
 // dup: this warp's 64-entry scratch (RM == 1), pm: the x argsort (debug dump only).
-template <int K, int RM, int G, bool SWEEP>
+// PARTIAL: when 32 does not divide n, scan only the existing members of the last chunk /
+// own block (the warp kernel, n < 128, where that chunk is a large share of the work); the CTA
+// kernel scans the +inf-padded chunk as a full one (identical results: +inf never enters).
+template <int K, int RM, int G, bool SWEEP, bool PARTIAL>
 __device__ __forceinline__ void ksg_block(const float2* __restrict__ xy, const float* __restrict__ sy,
                                           float2* __restrict__ dup, int n, int nch, int log2p, int mb, int lane,
                                           int k, const double* __restrict__ psi, int off, double& acc,
@@ -334,19 +362,28 @@ __device__ __forceinline__ void ksg_block(const float2* __restrict__ xy, const f
   }
   const int c0 = mb * RM;
   const int c1 = min(c0 + RM, nch);
+  const int vown = min(32, n - c0 * 32);  // members in the own chunk
   if constexpr (RM == 1) {
-    const float2 zc = xy[c0 * 32 + lane];
-    dup[lane] = zc;
-    dup[lane + 32] = zc;
-    __syncwarp();
-    own_rotated<K>(dup, lane, zi[0], l[0]);
+    if (!PARTIAL || vown == 32) {
+      const float2 zc = xy[c0 * 32 + lane];
+      dup[lane] = zc;
+      dup[lane + 32] = zc;
+      __syncwarp();
+      own_rotated<K>(dup, lane, zi[0], l[0]);
+    } else {
+      dup[lane] = xy[c0 * 32 + lane % vown];
+      dup[lane + 32] = xy[c0 * 32 + (lane + 32) % vown];
+      __syncwarp();
+      own_rotated_part<K>(dup, lane, zi[0], l[0], vown);
+    }
     __syncwarp();
   } else {
     OwnBlock<K, RM, RM - 1>::run(xy4, c0, nch, zi, l, lane);
   }
   // outward in chunks of 32 j; below descending, above ascending
   const int nh = nch;
-  int nproc = c1 - c0;
+  // executed comparisons per valid member: the own block's others + every scanned candidate
+  int ncand = (RM == 1) ? vown - 1 : min(BLK, n - c0 * 32) - 1;
   int hlo = c0 - 1, hhi = c1;
   while (hlo >= 0 || hhi < nh) {
     // SWEEP: per-member exact test -- member i still needs the chunk iff the x-gap to the
@@ -364,10 +401,10 @@ __device__ __forceinline__ void ksg_block(const float2* __restrict__ xy, const f
       if (!need) {
         hlo = -1;
       } else {
-        if (hlo == c0 - 1) chunk_plain<K, RM>(xy4 + hlo * 16, zi, l);
-        else chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l);
+        if (hlo == c0 - 1) chunk_plain<K, RM>(xy4 + hlo * 16, zi, l, 32);
+        else chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l, 32);
+        ncand += 32;
         --hlo;
-        ++nproc;
       }
     }
     if (hhi < nh) {
@@ -382,15 +419,16 @@ __device__ __forceinline__ void ksg_block(const float2* __restrict__ xy, const f
       if (!need) {
         hhi = nh;
       } else {
-        if (hhi == c1) chunk_plain<K, RM>(xy4 + hhi * 16, zi, l);
-        else chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l);
+        const int cnt = min(32, n - hhi * 32);
+        if (hhi == c1) chunk_plain<K, RM>(xy4 + hhi * 16, zi, l, PARTIAL ? cnt : 32);
+        else chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l, PARTIAL ? cnt : 32);
+        ncand += cnt;
         ++hhi;
-        ++nproc;
       }
     }
   }
   const int valid = min(BLK, n - mb * BLK);
-  if (lane == 0) executed += (unsigned long long)nproc * 32ull * (unsigned long long)valid;
+  if (lane == 0) executed += (unsigned long long)ncand * (unsigned long long)valid;
 #pragma unroll
   for (int rr = 0; rr < RM; ++rr) {
     if (ts[rr] < n) {
@@ -510,7 +548,7 @@ __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? 8
     double acc = 0.0;
     // member blocks: first one static, then dynamic (sweep lengths differ per block)
     for (int mb = warp; mb < nblk;) {
-      ksg_block<K, RM, G, SWEEP>(xy, sy, dupbuf + warp * 64, n, nch, log2p, mb, lane, k, psi, off, acc, executed,
+      ksg_block<K, RM, G, SWEEP, false>(xy, sy, dupbuf + warp * 64, n, nch, log2p, mb, lane, k, psi, off, acc, executed,
                                  out, u, pm, swap);
       int nb = 0;
       if (lane == 0) nb = atomicAdd(next_blk, 1);
@@ -673,7 +711,7 @@ __global__ void __launch_bounds__(128, 8) ksg_warp_kernel(
     __syncwarp();
     double acc = 0.0;
     for (int mb = 0; mb < nblk; ++mb)
-      ksg_block<K, 1, 4, SWEEP>(xy, sy, dup, n, nch, log2p, mb, lane, k, psi, off, acc, executed, out, u, pm, swap);
+      ksg_block<K, 1, 4, SWEEP, true>(xy, sy, dup, n, nch, log2p, mb, lane, k, psi, off, acc, executed, out, u, pm, swap);
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
