@@ -458,3 +458,25 @@ def test_shards_bit_identical_to_unsharded():
                 ms.append(m)
                 as_.append(a)
             assert torch.equal(torch.cat(ms), full_m) and torch.equal(torch.cat(as_), full_a)
+
+
+@pytest.mark.parametrize("n", [33, 34, 63, 65, 96, 97, 127, 128])
+def test_warp_kernel_partial_chunks(n):
+    """n < 128 runs one warp per pair (ksg_warp_kernel) and scans only the existing members of the
+    partial last chunk / own block (n = 33: one member, 63: 31); n = 128 is the first CTA-kernel
+    size.  eps / counts bit-exact, MI within tolerance, sweep == dense bit for bit."""
+    spec = synth.field_spec(8, 4, 2, n, seed=7 * n)
+    vals, f = _field(spec)
+    a, b = synth.random_pairs(spec.points, 200, seed=n)
+    a, b = a.numpy(), b.numpy()
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    for k in (1, 3, 8):
+        _check_knn(f, vals, k, a, b)
+        got = _cpu(cb.corr_eval_pairs(f, None, cb.CORR_KSG, k, ta, tb))
+        dense = _cpu(cb.corr_eval_pairs(f, None, cb.CORR_KSG | cb.CORR_F_KSG_DENSE, k, ta, tb))
+        ref = oracle.eval_pairs(vals.cpu(), None, oracle.KSG, k, a, b)
+        assert np.array_equal(got, dense, equal_nan=True)
+        assert np.array_equal(np.isnan(got), np.isnan(ref))
+        ok = ~np.isnan(ref)
+        assert np.max(np.abs(got[ok] - ref[ok]), initial=0) <= KSG_TOL
+    f.close()
