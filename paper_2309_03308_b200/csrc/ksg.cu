@@ -343,11 +343,11 @@ __device__ __forceinline__ bool peek_pair(const PairSrc& s, int64_t u, int64_t& 
 // own block (the warp kernel, n < 128, where that chunk is a large share of the work); the CTA
 // kernel scans the +inf-padded chunk as a full one (identical results: +inf never enters).
 template <int K, int RM, int G, bool SWEEP, bool PARTIAL>
-__device__ __forceinline__ void ksg_block(const float2* __restrict__ xy, const float* __restrict__ sy,
+__device__ __forceinline__ int ksg_block(const float2* __restrict__ xy, const float* __restrict__ sy,
                                           float2* __restrict__ dup, int n, int nch, int log2p, int mb, int lane,
                                           int k, const double* __restrict__ psi, int off, double& acc,
                                           unsigned long long& executed, const PairOut& out, int64_t u,
-                                          const uint16_t* __restrict__ pm, bool swap) {
+                                          const uint16_t* __restrict__ pm, bool swap, int* next_blk) {
   constexpr int BLK = 32 * RM;
   const float4* xy4 = reinterpret_cast<const float4*>(xy);
   float2 zi[RM];
@@ -428,7 +428,13 @@ __device__ __forceinline__ void ksg_block(const float2* __restrict__ xy, const f
     }
   }
   const int valid = min(BLK, n - mb * BLK);
-  if (lane == 0) executed += (unsigned long long)ncand * (unsigned long long)valid;
+  // claim the warp's next member block now (CTA kernel): the shared atomic's latency hides under
+  // the count searches
+  int nb = 0;
+  if (lane == 0) {
+    executed += (unsigned long long)ncand * (unsigned long long)valid;
+    if (next_blk) nb = atomicAdd(next_blk, 1);
+  }
 #pragma unroll
   for (int rr = 0; rr < RM; ++rr) {
     if (ts[rr] < n) {
@@ -449,6 +455,7 @@ __device__ __forceinline__ void ksg_block(const float2* __restrict__ xy, const f
       }
     }
   }
+  return __shfl_sync(0xffffffffu, nb, 0);
 }
 
 template <int K, int RM, int G, bool SWEEP>
@@ -548,11 +555,8 @@ __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? 8
     double acc = 0.0;
     // member blocks: first one static, then dynamic (sweep lengths differ per block)
     for (int mb = warp; mb < nblk;) {
-      ksg_block<K, RM, G, SWEEP, false>(xy, sy, dupbuf + warp * 64, n, nch, log2p, mb, lane, k, psi, off, acc, executed,
-                                 out, u, pm, swap);
-      int nb = 0;
-      if (lane == 0) nb = atomicAdd(next_blk, 1);
-      mb = __shfl_sync(0xffffffffu, nb, 0);
+      mb = ksg_block<K, RM, G, SWEEP, false>(xy, sy, dupbuf + warp * 64, n, nch, log2p, mb, lane, k, psi, off, acc,
+                                             executed, out, u, pm, swap, next_blk);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -711,7 +715,8 @@ __global__ void __launch_bounds__(128, 8) ksg_warp_kernel(
     __syncwarp();
     double acc = 0.0;
     for (int mb = 0; mb < nblk; ++mb)
-      ksg_block<K, 1, 4, SWEEP, true>(xy, sy, dup, n, nch, log2p, mb, lane, k, psi, off, acc, executed, out, u, pm, swap);
+      ksg_block<K, 1, 4, SWEEP, true>(xy, sy, dup, n, nch, log2p, mb, lane, k, psi, off, acc, executed, out, u, pm, swap,
+                                      nullptr);
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
