@@ -31,4 +31,16 @@ for rep in range(2):
     f = cb.corr_field_create(host, spec.nx, spec.ny, spec.nz, spec.members, device=0)
     res["create_from_pinned_host_s"] = time.perf_counter() - t
     f.close()
+# in-place re-ingest (corr_field_update: transpose, fp64 stats, tf32 split, per-row sort), CUDA events
+f = cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members)
+cb.corr_field_update(f, vals)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(3):
+    cb.corr_field_update(f, vals)
+e1.record()
+torch.cuda.synchronize()
+res["update_device_ms"] = e0.elapsed_time(e1) / 3
+f.close()
 print(json.dumps(res))
