@@ -25,7 +25,13 @@ __global__ void __launch_bounds__(256) bench(float* out, int iters, long long* c
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      if (OP == 0) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[c]) : "f"(b[c]));
+      // alternating max / min on the same chain: ptxas cannot fold two of them into one FMNMX3
+      // (a max-max pair on one register IS folded, which made an earlier version of this test
+      // report twice the real FMNMX rate)
+      if (OP == 0) {
+        asm volatile("max.f32 %0, %0, %1;" : "+f"(a[c]) : "f"(b[c]));
+        asm volatile("min.f32 %0, %0, %1;" : "+f"(a[c]) : "f"(b[(c + 1) % CH]));
+      }
       if (OP == 1) asm volatile("max.f32 %0, %0, %1, %2;" : "+f"(a[c]) : "f"(b[c]), "f"(b[(c + 1) % CH]));
       if (OP == 2) asm volatile("add.rn.f32 %0, %0, %1;" : "+f"(a[c]) : "f"(b[c]));
       if (OP == 3) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(p[c]) : "l"(q));
@@ -49,6 +55,10 @@ __global__ void __launch_bounds__(256) bench(float* out, int iters, long long* c
         asm volatile("{.reg .pred q; setp.lt.f32 q, %0, %1; @q add.u32 %2, %2, 1;}" : "+f"(a[c]), "+f"(b[c]), "+r"(u[c]));
       }
       if (OP == 10) asm volatile("min.u32 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 1) % CH]));
+      if (OP == 11) {  // the merge network's shape: min(l, max(l', a)) pairs
+        asm volatile("max.f32 %0, %1, %2;" : "=f"(b[c]) : "f"(a[c]), "f"(a[(c + 1) % CH]));
+        asm volatile("min.f32 %0, %0, %1;" : "+f"(a[c]) : "f"(b[c]));
+      }
     }
   }
   long long t1 = clock64();
@@ -93,7 +103,7 @@ int main() {
   float* d_out; long long* d_cyc;
   cudaMalloc(&d_out, blocks * threads * sizeof(float));
   cudaMalloc(&d_cyc, blocks * sizeof(long long));
-  run<0>("FMNMX", 1, d_out, d_cyc, blocks, threads, iters);
+  run<0>("FMNMX", 2, d_out, d_cyc, blocks, threads, iters);
   run<1>("FMNMX3", 1, d_out, d_cyc, blocks, threads, iters);
   run<2>("FADD", 1, d_out, d_cyc, blocks, threads, iters);
   run<3>("FADD2", 1, d_out, d_cyc, blocks, threads, iters);
@@ -104,6 +114,7 @@ int main() {
   run<8>("FFMA+FMNMX", 2, d_out, d_cyc, blocks, threads, iters);
   run<9>("FSETP+@IADD", 2, d_out, d_cyc, blocks, threads, iters);
   run<10>("IMNMX", 1, d_out, d_cyc, blocks, threads, iters);
+  run<11>("FMNMX max->min pairs", 2, d_out, d_cyc, blocks, threads, iters);
   cudaError_t e = cudaGetLastError();
   printf("{\"status\": \"%s\"}\n", cudaGetErrorString(e));
   return 0;
