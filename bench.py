@@ -205,6 +205,7 @@ def main():
     ap.add_argument("--cpu-pairs", type=int, default=768)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense-pass reference roofline")
     ap.add_argument("--workload", default="c4", choices=["c4", "c3"],
                     help="c4 = the BASELINE metric's config (default); c3 (n=100) only for dry runs")
     args = ap.parse_args()
@@ -341,20 +342,22 @@ def main():
                 "ksg_ms_per_step": ksg_ms, "algorithmic_bytes_per_pair": 14 * spec.members}
     # the same kernel with the sweep disabled (CORR_F_KSG_DENSE): all n(n-1) comparisons executed,
     # results bit-identical -- the ALU-efficiency reference for the dense k-NN pass
-    Sd = 256
-    cb.corr_ksg_comparisons(local, reset=True)
-    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    d0.record(stream)
-    cb.corr_region_max(field, None, cb.CORR_KSG | cb.CORR_F_KSG_DENSE, K_NN, Ash, Bsh, Sd, SEED)
-    d1.record(stream)
-    torch.cuda.synchronize()
-    dense_s = d0.elapsed_time(d1) / 1e3
-    dense_exec = cb.corr_ksg_comparisons(local, reset=True)
-    roofline_dense = {"bound": "alu", "kernel": "ksg_sorted_kernel<3,1,dense> (CORR_F_KSG_DENSE)",
-                      "achieved": (hi - lo) * Sd * n * (n - 1) / dense_s / 1e9, "peak": peak / 1e9, "unit": "Gcmp/s",
-                      "frac": (hi - lo) * Sd * n * (n - 1) / dense_s / peak,
-                      "executed_comparisons_per_pair": dense_exec / max((hi - lo) * Sd, 1),
-                      "pairs_per_s": (hi - lo) * Sd / dense_s, "sample": f"{hi - lo} region pairs x {Sd} samples"}
+    roofline_dense = None
+    if not args.no_dense:
+        Sd = 256
+        cb.corr_ksg_comparisons(local, reset=True)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        cb.corr_region_max(field, None, cb.CORR_KSG | cb.CORR_F_KSG_DENSE, K_NN, Ash, Bsh, Sd, SEED)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        dense_s = d0.elapsed_time(d1) / 1e3
+        dense_exec = cb.corr_ksg_comparisons(local, reset=True)
+        roofline_dense = {"bound": "alu", "kernel": "ksg_sorted_kernel<3,4,4,dense> (CORR_F_KSG_DENSE, 4 members per lane)",
+                          "achieved": (hi - lo) * Sd * n * (n - 1) / dense_s / 1e9, "peak": peak / 1e9, "unit": "Gcmp/s",
+                          "frac": (hi - lo) * Sd * n * (n - 1) / dense_s / peak,
+                          "executed_comparisons_per_pair": dense_exec / max((hi - lo) * Sd, 1),
+                          "pairs_per_s": (hi - lo) * Sd / dense_s, "sample": f"{hi - lo} region pairs x {Sd} samples"}
     # secondary: the focus-block GEMM (tensor-bound) and the sampled Pearson pairs (HBM/L2-bound)
     fa_box, fb_box = slabs[rank], fB
     nA = (fa_box[3] - fa_box[0]) * (fa_box[4] - fa_box[1]) * (fa_box[5] - fa_box[2])
@@ -401,22 +404,28 @@ def main():
                 cdist.replicate_field_sharded(host, bufs[slot], rank, world, group=bgroup)
                 cb.corr_field_update(slots[slot], bufs[slot], stream=up)
 
+        step_evs = []
+
         def run_e2e(nsteps):
             nonlocal pinned_out
             done = [None, None]
+            step_evs.clear()
             upload(0)
             for i in range(nsteps):
                 s_ = i % 2
                 stream.wait_stream(up)
+                e_a = torch.cuda.Event(enable_timing=True)
+                e_a.record(stream)
                 out = step(slots[s_])
                 if pinned_out is None:
                     pinned_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in out]
                 for dst, o in zip(pinned_out, out):
                     dst.copy_(o, non_blocking=True)
                 d2h_holder[0] = sum(o.numel() * o.element_size() for o in out)
-                ev = torch.cuda.Event()
+                ev = torch.cuda.Event(enable_timing=True)
                 ev.record(stream)
                 done[s_] = ev
+                step_evs.append((e_a, ev))
                 if i + 1 < nsteps:
                     upload((i + 1) % 2, after=done[(i + 1) % 2])
             torch.cuda.synchronize()
@@ -440,6 +449,7 @@ def main():
             h2d = int(hb[0])
         e2e = {"value": total_pairs / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h_holder[0], "s_per_step": e_s,
+               "device_step_ms": [round(a.elapsed_time(b), 1) for a, b in step_evs],
                "includes": "per step: pinned-host upload of the 7.04 GB field (1/N of the member rows per "
                             "rank, exchanged by NCCL broadcasts), "
                            "corr_field_update ingest, the step, D2H of the maxima; double-buffered "

@@ -218,6 +218,15 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
   DeviceGuard guard(device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  {
+    // the per-call scratch (region tables, key arrays) comes from the stream-ordered pool: keep
+    // freed blocks mapped instead of returning them to the OS at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = 64ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
 
   corr_field* f = nullptr;
   const int arc = alloc_field(nx, ny, nz, members, device, st, &f);
