@@ -792,6 +792,10 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int pl
                             : launch_t<16, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   if (k <= 24) return sweep ? launch_t<24, 1, 4, true>(fa, fb, k, plus1, src, out, st)
                             : launch_t<24, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  // k = 30 is the paper's rule ceil(3n/100) at n = 1000 (Table 1): an exact-size list keeps the
+  // filter/sweep threshold at l[k-1] itself and saves 2 of 32 merge lanes
+  if (k == 30) return sweep ? launch_t<30, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<30, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   if (k <= 32) return sweep ? launch_t<32, 1, 4, true>(fa, fb, k, plus1, src, out, st)
                             : launch_t<32, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   return cudaErrorNotSupported;
