@@ -458,6 +458,140 @@ __device__ __forceinline__ int ksg_block(const float2* __restrict__ xy, const fl
   return __shfl_sync(0xffffffffu, nb, 0);
 }
 
+
+// ---- large k (the paper's k = ceil(3n/100), e.g. 30 at n = 1000): batched exact updates ------
+// With a 32-entry list the 2-value merge network costs ~3K min/max per pair of values.  Here a
+// whole 32-candidate chunk is merged at once: the lane's 32 distances are sorted by a bitonic
+// network (240 compare-exchanges) and merged with the sorted list by the half-cleaner
+// c_i = min(l_i, d_{31-i}) (the 32 smallest of both, as a bitonic sequence) followed by a
+// 5-stage bitonic merge: ~21 min/max per value instead of ~48.  The list INCLUDES the member
+// itself (d_ii = 0), so eps_i = l[k] -- the (k+1)-th smallest over all j, identical to the
+// k-th over j != i (R3).  Chunks whose distances are all >= l[KT] (KT = k, compile-time) are
+// skipped (exact: they cannot change the k+1 smallest); the sweep uses the same threshold.
+__device__ __forceinline__ void cas_asc(float& a, float& b) {
+  const float lo = fminf(a, b), hi = fmaxf(a, b);
+  a = lo;
+  b = hi;
+}
+
+__device__ __forceinline__ void bitonic_sort32(float (&d)[32]) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int j = i ^ stride;
+        if (j > i) {
+          if ((i & size) == 0) cas_asc(d[i], d[j]);
+          else cas_asc(d[j], d[i]);
+        }
+      }
+    }
+  }
+}
+
+// l (sorted, 32) <- the 32 smallest of l and d (d is destroyed)
+__device__ __forceinline__ void batch_merge32(float (&l)[32], float (&d)[32]) {
+  bitonic_sort32(d);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) l[i] = fminf(l[i], d[31 - i]);
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int j = i ^ stride;
+      if (j > i) cas_asc(l[i], l[j]);
+    }
+  }
+}
+
+template <int KT, bool SWEEP>
+__device__ __forceinline__ int ksg_block_big(const float2* __restrict__ xy, const float* __restrict__ sy, int n,
+                                             int nch, int log2p, int mb, int lane, int k,
+                                             const double* __restrict__ psi, int off, double& acc,
+                                             unsigned long long& executed, const PairOut& out, int64_t u,
+                                             const uint16_t* __restrict__ pm, bool swap, int* next_blk) {
+  const int ti = mb * 32 + lane;
+  const float2 zi = xy[ti];
+  float l[32];
+#pragma unroll
+  for (int t = 0; t < 32; ++t) l[t] = INFINITY;
+  const float4* xy4 = reinterpret_cast<const float4*>(xy);
+  const int c0 = mb, c1 = mb + 1;
+  int ncand = min(32, n - c0 * 32) - 1;
+  // chunk sequence: own block (exact), then below / above alternately; the first chunk in each
+  // direction is merged unconditionally, later ones only if some lane has a candidate < l[KT]
+  int hlo = c0 - 1, hhi = c1, dir = 1;
+  int h = c0;
+  bool exact = true;
+#pragma unroll 1
+  while (true) {
+    float d[32];
+    const float4* cp = xy4 + h * 16;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const float4 v = cp[q];
+      d[2 * q] = cheb(zi, make_float2(v.x, v.y));
+      d[2 * q + 1] = cheb(zi, make_float2(v.z, v.w));
+    }
+    bool merge = exact;
+    if (!merge) {
+      float m = d[0];
+#pragma unroll
+      for (int q = 1; q < 32; ++q) m = fminf(m, d[q]);
+      merge = __any_sync(0xffffffffu, m < l[KT]);
+    }
+    if (merge) batch_merge32(l, d);
+    if (h != c0) ncand += min(32, n - h * 32);
+    // next chunk: alternate directions; a direction ends at the array edge or by the sweep test
+    bool found = false;
+#pragma unroll 1
+    for (int tries = 0; tries < 2 && !found; ++tries) {
+      dir ^= 1;
+      const int hc = dir ? hhi : hlo;
+      if (dir ? hc >= nch : hc < 0) continue;
+      bool need = true;
+      if (SWEEP) {
+        const float xe = xy[hc * 32 + (dir ? 0 : 31)].x;
+        const float gap = dir ? xe - zi.x : zi.x - xe;
+        need = __any_sync(0xffffffffu, (ti < n) && (gap < l[KT]));
+      }
+      if (!need) {
+        if (dir) hhi = nch; else hlo = -1;
+        continue;
+      }
+      exact = dir ? (hc == c1) : (hc == c0 - 1);
+      h = hc;
+      if (dir) ++hhi; else --hlo;
+      found = true;
+    }
+    if (!found) break;
+  }
+  const int valid = min(32, n - mb * 32);
+  int nb = 0;
+  if (lane == 0) {
+    executed += (unsigned long long)ncand * (unsigned long long)valid;
+    if (next_blk) nb = atomicAdd(next_blk, 1);
+  }
+  if (ti < n) {
+    float e = l[0];
+#pragma unroll
+    for (int t = 1; t < 32; ++t)
+      if (t == k) e = l[t];  // (k+1)-th smallest including the member itself
+    int cu, cv;
+    marginal_counts(xy, sy, log2p, zi.x, zi.y, e, cu, cv);
+    acc += __ldg(psi + cu + off) + __ldg(psi + cv + off);
+    if (out.dbg_eps) {
+      const int m = pm[ti];
+      out.dbg_eps[u * n + m] = e;
+      out.dbg_nx[u * n + m] = swap ? cv : cu;
+      out.dbg_ny[u * n + m] = swap ? cu : cv;
+    }
+  }
+  return __shfl_sync(0xffffffffu, nb, 0);
+}
+
 template <int K, int RM, int G, bool SWEEP>
 __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? 8 : 3))) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
@@ -555,8 +689,15 @@ __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? 8
     double acc = 0.0;
     // member blocks: first one static, then dynamic (sweep lengths differ per block)
     for (int mb = warp; mb < nblk;) {
-      mb = ksg_block<K, RM, G, SWEEP, false>(xy, sy, dupbuf + warp * 64, n, nch, log2p, mb, lane, k, psi, off, acc,
-                                             executed, out, u, pm, swap, next_blk);
+      if constexpr (RM == 1 && (K == 30 || K == 31)) {
+        // batched 32-entry lists including the member itself: K is the threshold index l[K]
+        // (K = 30 for the paper's k = 30; K = 31 serves 24 < k <= 31)
+        mb = ksg_block_big<K, SWEEP>(xy, sy, n, nch, log2p, mb, lane, k, psi, off, acc, executed,
+                                                      out, u, pm, swap, next_blk);
+      } else {
+        mb = ksg_block<K, RM, G, SWEEP, false>(xy, sy, dupbuf + warp * 64, n, nch, log2p, mb, lane, k, psi, off,
+                                               acc, executed, out, u, pm, swap, next_blk);
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -792,10 +933,12 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int pl
                             : launch_t<16, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   if (k <= 24) return sweep ? launch_t<24, 1, 4, true>(fa, fb, k, plus1, src, out, st)
                             : launch_t<24, 1, 4, false>(fa, fb, k, plus1, src, out, st);
-  // k = 30 is the paper's rule ceil(3n/100) at n = 1000 (Table 1): an exact-size list keeps the
-  // filter/sweep threshold at l[k-1] itself and saves 2 of 32 merge lanes
+  // 24 < k <= 31 (k = 30 is the paper's rule ceil(3n/100) at n = 1000, Table 1): batched
+  // 32-entry lists (ksg_block_big); k = 30 gets its own threshold index l[30]
   if (k == 30) return sweep ? launch_t<30, 1, 4, true>(fa, fb, k, plus1, src, out, st)
                             : launch_t<30, 1, 4, false>(fa, fb, k, plus1, src, out, st);
+  if (k <= 31) return sweep ? launch_t<31, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+                            : launch_t<31, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   if (k <= 32) return sweep ? launch_t<32, 1, 4, true>(fa, fb, k, plus1, src, out, st)
                             : launch_t<32, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   return cudaErrorNotSupported;

@@ -80,7 +80,8 @@ def test_c1_eps_counts_bit_exact():
                                       (130, 5, (8, 8, 2)), (257, 8, (8, 4, 2)), (1001, 4, (4, 4, 2)),
                                       (4, 3, (8, 8, 1)), (129, 2, (8, 4, 2)), (1000, 30, (4, 4, 2)),
                                       (200, 12, (8, 4, 2)), (300, 17, (8, 4, 2)), (1000, 0, (4, 4, 2)),
-                                      (64, 32, (8, 4, 2))])
+                                      (64, 32, (8, 4, 2)), (500, 31, (4, 4, 2)), (700, 25, (4, 4, 2)),
+                                      (129, 30, (4, 4, 2))])
 def test_eps_counts_mi_bit_exact_ragged(n, k, dims):
     """k = 0 selects the paper's ceil(3n/100); k > 8 uses the long-list kernels."""
     spec = synth.field_spec(*dims, n, seed=100 + n)
