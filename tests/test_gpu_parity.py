@@ -481,3 +481,26 @@ def test_warp_kernel_partial_chunks(n):
         ok = ~np.isnan(ref)
         assert np.max(np.abs(got[ok] - ref[ok]), initial=0) <= KSG_TOL
     f.close()
+
+
+@pytest.mark.parametrize("k", [30, 31])
+def test_batched_large_k_two_fields_and_dense(k):
+    """The batched 32-list path (24 < k <= 31) on TWO fields (x from one variable, y from the
+    other; the sort marginal swaps per pair) and with CORR_F_KSG_DENSE: eps / counts bit-exact,
+    sweep == dense bit for bit."""
+    n = 1000
+    sa = synth.field_spec(4, 4, 2, n, seed=11)
+    sb = synth.field_spec(4, 4, 2, n, seed=12, variable=2)
+    va, fa = _field(sa)
+    vb, fb = _field(sb)
+    a, b = synth.random_pairs(sa.points, 24, seed=k)
+    a, b = a.numpy(), b.numpy()
+    _check_knn(fa, va, k, a, b, fb=fb, vals_b=vb)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    got = _cpu(cb.corr_eval_pairs(fa, fb, cb.CORR_KSG, k, ta, tb))
+    dense = _cpu(cb.corr_eval_pairs(fa, fb, cb.CORR_KSG | cb.CORR_F_KSG_DENSE, k, ta, tb))
+    ref = oracle.eval_pairs(va.cpu(), vb.cpu(), oracle.KSG, k, a, b)
+    assert np.array_equal(got, dense, equal_nan=True)
+    assert np.max(np.abs(got - ref)) <= KSG_TOL
+    fa.close()
+    fb.close()
