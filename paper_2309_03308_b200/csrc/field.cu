@@ -153,32 +153,63 @@ __global__ void __launch_bounds__(512) sort_kernel(const float* __restrict__ F, 
 
 // ---- 3b. per-row radix sort (one CTA of T threads x I items per row, N2 = T*I) ------
 // The bitonic network above costs log2(N2)(log2(N2)+1)/2 shared-memory passes with a
-// barrier each (55 at n = 1000); an LSD radix sort of order-preserving u32 keys needs 8
-// 4-bit passes.  Keys: u = bits(f); u ^= (u >> 31 ? 0xFFFFFFFF : 0x80000000) (finite
+// barrier each (55 at n = 1000); an LSD radix sort of order-preserving u32 keys needs at
+// most 8 4-bit passes.  Keys: u = bits(f); u ^= (u >> 31 ? 0xFFFFFFFF : 0x80000000) (finite
 // inputs, checked at ingest), so u32 order == float order (-0 before +0; equal floats
 // compare equal in every consumer, and KSG only needs SOME sorted permutation, R4).
-// Values: the member index.  Rows are loaded striped (coalesced) and written striped.
+// Only the key bits that vary within the row are sorted: all keys lie in [kmin, kmax], so
+// they share every bit above the highest bit where kmin and kmax differ (ensemble rows share
+// sign, exponent and leading mantissa bits: typically 5 passes instead of 8).  The row is
+// loaded BLOCKED (thread t holds members t*I .. t*I+I-1), the padding slots e >= n get key kmax
+// and sit at the highest blocked positions, so the stable sort leaves them last.  Values: the
+// member index.  Output is written striped (coalesced).
 template <int T, int I>
 __global__ void __launch_bounds__(T) sort_radix_kernel(const float* __restrict__ F, float* __restrict__ S,
                                                        uint16_t* __restrict__ perm, int n, int n_pad, int64_t P) {
   using Sorter = cub::BlockRadixSort<uint32_t, T, I, uint16_t>;
   __shared__ typename Sorter::TempStorage tmp;
+  __shared__ uint32_t kext[2];  // min and max key of the row
   for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
     const float* row = F + p * n_pad;
     uint32_t key[I];
     uint16_t idx[I];
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
 #pragma unroll
     for (int i = 0; i < I; ++i) {
-      const int e = i * T + (int)threadIdx.x;
-      uint32_t u = 0xFFFFFFFFu;  // +inf pad sorts last (its key is below 0xFFFFFFFF: never equal)
+      const int e = (int)threadIdx.x * I + i;
+      uint32_t u = 0u;
       if (e < n) {
         u = __float_as_uint(row[e]);
         u ^= (u >> 31) ? 0xFFFFFFFFu : 0x80000000u;
+        kmin = min(kmin, u);
+        kmax = max(kmax, u);
       }
       key[i] = u;
       idx[i] = (uint16_t)(e < n ? e : 0xFFFF);
     }
-    Sorter(tmp).SortBlockedToStriped(key, idx);
+    if (threadIdx.x == 0) {
+      kext[0] = 0xFFFFFFFFu;
+      kext[1] = 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&kext[0], kmin);
+      atomicMax(&kext[1], kmax);
+    }
+    __syncthreads();
+    kmin = kext[0];
+    kmax = kext[1];
+#pragma unroll
+    for (int i = 0; i < I; ++i)
+      if ((int)threadIdx.x * I + i >= n) key[i] = kmax;
+    const uint32_t diff = kmin ^ kmax;
+    const int end_bit = diff ? 32 - __clz(diff) : 1;  // a constant row still goes through one pass
+    Sorter(tmp).SortBlockedToStriped(key, idx, 0, end_bit);
 #pragma unroll
     for (int i = 0; i < I; ++i) {
       const int e = i * T + (int)threadIdx.x;
@@ -189,7 +220,7 @@ __global__ void __launch_bounds__(T) sort_radix_kernel(const float* __restrict__
         perm[p * n_pad + e] = e < n ? idx[i] : (uint16_t)0xFFFF;
       }
     }
-    __syncthreads();  // tmp is reused by the next row
+    __syncthreads();  // tmp / kext are reused by the next row
   }
 }
 
