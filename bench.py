@@ -363,10 +363,16 @@ def main():
     nA = (fa_box[3] - fa_box[0]) * (fa_box[4] - fa_box[1]) * (fa_box[5] - fa_box[2])
     nB = (fb_box[3] - fb_box[0]) * (fb_box[4] - fb_box[1]) * (fb_box[5] - fb_box[2])
     tf32_peak = (peaks.get("bf16_tflops") or 1664.4) * 0.5
+    tf32_ctx = None  # cuBLAS TF32 GEMM measured on this pool (profiles/r01_tf32_peak.json), context only
+    try:
+        tf32_ctx = json.load(open(os.path.join(ROOT, "profiles", "r01_tf32_peak.json")))["tf32_tflops_burst"]
+    except Exception:
+        pass
     blk_tflops = 3 * 2.0 * nA * nB * n / (stage_ms["pearson_block"] / 1e3) / 1e12
     roofline_block = {"bound": "tensor", "kernel": "pearson_block_kernel (tcgen05 kind::tf32, 3 MMAs/k-step)",
                       "achieved": blk_tflops, "peak": tf32_peak, "unit": "TFLOP/s", "frac": blk_tflops / tf32_peak,
                       "peak_basis": "measured bf16 dense x 0.5 (nominal tf32:bf16 ratio)",
+                      "cublas_tf32_measured": tf32_ctx,
                       "pairs_per_s": nA * nB / (stage_ms["pearson_block"] / 1e3),
                       "ms_per_step": stage_ms["pearson_block"]}
     ps_gbs = my_pairs * (8 * spec.n_pad if hasattr(spec, "n_pad") else 8 * ((n + 7) // 8 * 8)) / (
