@@ -203,6 +203,18 @@ int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset) {
   return CORR_OK;
 }
 
+int corr_gemm_flops(int32_t device, int64_t* flops, int32_t reset) {
+  if (!flops) return fail(CORR_E_INVAL, "flops is NULL");
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long v = 0;
+  if (e == cudaSuccess) e = gemm_flops(&v, reset != 0);
+  if (e != cudaSuccess) return cuda_fail(e, "corr_gemm_flops");
+  *flops = (int64_t)v;
+  return CORR_OK;
+}
+
 int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t device,
                       void* cuda_stream, corr_field** out) {
   if (!out) return fail(CORR_E_INVAL, "out is NULL");

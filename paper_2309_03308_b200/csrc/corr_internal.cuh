@@ -75,6 +75,7 @@ cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int f
 cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1,
                        const PairSrc& src, const PairOut& out, cudaStream_t st);
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset);
+cudaError_t gemm_flops(unsigned long long* value, bool reset);
 cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
                                  const PairOut& out, cudaStream_t st);
 cudaError_t launch_region_finalize(const PairSrc& src, const unsigned long long* keys,

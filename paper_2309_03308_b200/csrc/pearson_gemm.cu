@@ -155,11 +155,28 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmRegion* __restrict__ r
   return c;
 }
 
+// Order-preserving u32 of a float (0 is reserved for "no value"; every real key is > 0).
+__device__ __forceinline__ uint32_t ord32(float v) {
+  uint32_t u = __float_as_uint(v + 0.0f);
+  return u ^ ((u >> 31) ? 0xFFFFFFFFu : 0x80000000u);
+}
+__device__ __forceinline__ float unord32(uint32_t u) {
+  return __uint_as_float(u ^ ((u >> 31) ? 0x80000000u : 0xFFFFFFFFu));
+}
+
+// SCREEN = true: the hi*hi product only (1 of the 3 MMAs, half the operand bytes); the epilogue
+// records each tile's masked maximum (tile_keys[t]) and each region pair's (reg_keys[r]).
+// SCREEN = false: the full split-TF32 product with the max/argmax epilogue, over the tile list
+// tlist[0 .. *tcount) (or every tile when tlist == nullptr).
+template <bool SCREEN>
 __global__ void __launch_bounds__(kThreads, 1)
     pearson_block_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                          const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                          const GemmRegion* __restrict__ reg, GemmGeom g, const uint8_t* __restrict__ ca,
-                         const uint8_t* __restrict__ cb, unsigned long long* __restrict__ keys) {
+                         const uint8_t* __restrict__ cb, unsigned long long* __restrict__ keys,
+                         const int* __restrict__ tlist, const int* __restrict__ tcount,
+                         uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ reg_keys) {
+  const int64_t ntiles = tlist ? (int64_t)*tcount : g.total_tiles;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-align the operand stages (128-byte swizzle atoms)
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -202,7 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mBhi) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mBlo) : "memory");
       uint32_t it = 0;
-      for (int64_t t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+      for (int64_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
+        const int64_t t = tlist ? (int64_t)tlist[i] : i;
         const TileCoord c = tile_coord(reg, g.nreg, t);
         const GemmRegion& R = reg[c.r];
         const int ax = R.A.x0 + c.tx * g.bxA, ay = R.A.y0 + c.ty * g.byA, az = R.A.z0 + c.tz * g.bzA;
@@ -211,18 +229,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           mbar_wait(empty + s, ph ^ 1);
           unsigned char* st = stage_base + s * STAGE_BYTES;
-          mbar_expect_tx(full + s, STAGE_BYTES);
+          mbar_expect_tx(full + s, SCREEN ? A_BYTES + B_BYTES : STAGE_BYTES);
           tma_load_4d(st, &mAhi, full + s, kb * BK, ax, ay, az);
-          tma_load_4d(st + A_BYTES, &mAlo, full + s, kb * BK, ax, ay, az);
+          if (!SCREEN) tma_load_4d(st + A_BYTES, &mAlo, full + s, kb * BK, ax, ay, az);
           tma_load_4d(st + 2 * A_BYTES, &mBhi, full + s, kb * BK, bx, by, bz);
-          tma_load_4d(st + 2 * A_BYTES + B_BYTES, &mBlo, full + s, kb * BK, bx, by, bz);
+          if (!SCREEN) tma_load_4d(st + 2 * A_BYTES + B_BYTES, &mBlo, full + s, kb * BK, bx, by, bz);
         }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     uint32_t it = 0, tt = 0;
-    for (int64_t t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++tt) {
+    for (int64_t i = blockIdx.x; i < ntiles; i += gridDim.x, ++tt) {
       const uint32_t acc = tt & 1, aph = (tt >> 1) & 1;
       mbar_wait(tempty + acc, aph ^ 1);
       tc_fence_after();
@@ -240,8 +258,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 bytes inside the swizzle atom
             const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
             tc_mma_tf32(dcol, dAhi + adv, dBhi + adv, kIdesc, first);
-            tc_mma_tf32(dcol, dAhi + adv, dBlo + adv, kIdesc, 1u);
-            tc_mma_tf32(dcol, dAlo + adv, dBhi + adv, kIdesc, 1u);
+            if (!SCREEN) {
+              tc_mma_tf32(dcol, dAhi + adv, dBlo + adv, kIdesc, 1u);
+              tc_mma_tf32(dcol, dAlo + adv, dBhi + adv, kIdesc, 1u);
+            }
           }
           tc_commit(empty + s);  // smem stage free once these MMAs have read it
         }
@@ -256,7 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q4 * 32 + lane;        // accumulator row = A point of the tile
     const int et = threadIdx.x - 64;       // 0..127
     uint32_t tt = 0;
-    for (int64_t t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++tt) {
+    for (int64_t i = blockIdx.x; i < ntiles; i += gridDim.x, ++tt) {
+      const int64_t t = tlist ? (int64_t)tlist[i] : i;
       const uint32_t acc = tt & 1, aph = (tt >> 1) & 1;
       const TileCoord c = tile_coord(reg, g.nreg, t);
       const GemmRegion& R = reg[c.r];
@@ -312,6 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         float m = v[0];
 #pragma unroll
         for (int i = 1; i < 32; ++i) m = fmaxf(m, v[i]);
+        if (SCREEN) {
+          best = fmaxf(best, m);
+          continue;
+        }
         if (m > best) {
           int j = 31;
 #pragma unroll
@@ -325,6 +350,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
+      if (SCREEN) {
+        uint32_t k32 = (row_ok && best > -INFINITY) ? ord32(best) : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) k32 = max(k32, __shfl_xor_sync(0xffffffffu, k32, o));
+        if (lane == 0 && k32 != 0u) {
+          atomicMax(tile_keys + t, k32);
+          atomicMax(reg_keys + c.r, k32);
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        continue;
+      }
       unsigned long long key = 0ULL;
       if (row_ok && best > -INFINITY) {
         best = fminf(1.f, fmaxf(-1.f, best));
@@ -773,6 +809,35 @@ cudaError_t launch_pearson_block2(const corr_field* fa, const corr_field* fb, co
   return e;
 }
 
+// executed tensor-core work of the block GEMMs (logical MMA flops incl. tile padding): the
+// roofline numerator of bench.py's Pearson block line (corr_gemm_flops)
+__device__ unsigned long long g_gemm_flops;
+
+__global__ void gemm_account_kernel(const int* __restrict__ tcount, long long tiles_screen, long long flop_per_mma_tile) {
+  const long long exact = tcount ? (long long)*tcount : 0;
+  atomicAdd(&g_gemm_flops, (unsigned long long)((tiles_screen + 3 * exact) * flop_per_mma_tile));
+}
+
+// screen -> tile list: keep tile t iff its approximate maximum is within delta of its region pair's
+// approximate maximum (tiles with no admissible entry, key 0, are dropped)
+
+__global__ void __launch_bounds__(256) screen_select_kernel(const GemmRegion* __restrict__ reg, int64_t nreg,
+                                                            int64_t tiles, const uint32_t* __restrict__ tile_keys,
+                                                            const uint32_t* __restrict__ reg_keys,
+                                                            int* __restrict__ tlist, int* __restrict__ tcount,
+                                                            float delta) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tiles; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = tile_keys[t];
+    if (k == 0u) continue;
+    int64_t lo = 0, hi = nreg - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (reg[mid].tile_off <= t) lo = mid; else hi = mid - 1;
+    }
+    if (unord32(k) >= unord32(reg_keys[lo]) - delta) tlist[atomicAdd(tcount, 1)] = (int)t;
+  }
+}
+
 cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, const RegionDev* hreg,
                                  const RegionDev* /*dreg*/, int64_t nreg, int absval, unsigned long long* keys,
                                  cudaStream_t st) {
@@ -835,17 +900,74 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   e = cudaMemcpyAsync(dgr, gr.data(), gr.size() * sizeof(GemmRegion), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16 + 2 * BN * 4 + 2 * BN * 4;
-  e = cudaFuncSetAttribute(pearson_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(pearson_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(pearson_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = kSMs;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = tiles < sms ? tiles : sms;
-  pearson_block_kernel<<<(unsigned)grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag,
-                                                               keys);
-  note_launch();
+  static const int noscreen = [] {
+    const char* v = getenv("CORR_GEMM_NOSCREEN");  // A/B switch: every tile through the full product
+    return (v && v[0] == '1') ? 1 : 0;
+  }();
+  const long long flop_tile = 2LL * BM * BN * (long long)(g.kblocks * BK);
+  if (noscreen || tiles >= (int64_t)INT32_MAX) {
+    pearson_block_kernel<false><<<(unsigned)grid, kThreads, smem, st>>>(
+        mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag, keys, nullptr, nullptr, nullptr, nullptr);
+    gemm_account_kernel<<<1, 1, 0, st>>>(nullptr, 3LL * tiles, flop_tile);
+    note_launch(2);
+    e = cudaGetLastError();
+    cudaFreeAsync(dgr, st);
+    return e;
+  }
+  // Screened two-pass evaluation (exact): pass 1 computes every tile with the hi*hi product only
+  // and records tile and region-pair maxima of that approximation; a tile can hold the region
+  // pair's maximum only if its approximate maximum is within kScreenDelta of the region pair's,
+  // so pass 2 runs the full split-TF32 product (and the max/argmax epilogue) on those tiles only.
+  // Bound on |pass-1 value - pass-2 value| for unit-norm rows (Cauchy-Schwarz):
+  //   split:        |z z' - hi hi'| summed <= (2 * 2^-11 + 2^-22) ||z|| ||z'||
+  //   accumulation: each pass adds K fp32 terms, error <= K * 2^-23 * sum|terms| (any order,
+  //                 truncating adds) -> 2 * K * 2^-23 for both passes together
+  // A tile whose approximate maximum is below (region approx max - 2b) holds only entries whose
+  // exact value is below the region's maximum, so dropping it changes neither max nor argmax.
+  const double b_bound = 2.0 * std::ldexp(1.0, -11) + std::ldexp(1.0, -22) +
+                         2.0 * (double)(g.kblocks * BK) * std::ldexp(1.0, -23) + 1e-6;
+  const float delta = (float)(2.0 * b_bound * 1.1);  // 10 % margin; 2.7e-3 at n = 1000
+  uint32_t* tile_keys = nullptr;
+  uint32_t* reg_keys = nullptr;
+  int* tlist = nullptr;
+  int* tcount = nullptr;
+  e = cudaMallocAsync((void**)&tile_keys, (size_t)tiles * 4, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&tlist, (size_t)tiles * 4, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&reg_keys, (size_t)nreg * 4 + 16, st);
+  if (e != cudaSuccess) return e;
+  tcount = reinterpret_cast<int*>(reg_keys + nreg);
+  cudaMemsetAsync(tile_keys, 0, (size_t)tiles * 4, st);
+  cudaMemsetAsync(reg_keys, 0, (size_t)nreg * 4 + 16, st);
+  pearson_block_kernel<true><<<(unsigned)grid, kThreads, smem, st>>>(
+      mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag, keys, nullptr, nullptr, tile_keys, reg_keys);
+  screen_select_kernel<<<(unsigned)std::min<int64_t>((tiles + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(
+      dgr, g.nreg, tiles, tile_keys, reg_keys, tlist, tcount, delta);
+  pearson_block_kernel<false><<<(unsigned)grid, kThreads, smem, st>>>(
+      mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag, keys, tlist, tcount, nullptr, nullptr);
+  gemm_account_kernel<<<1, 1, 0, st>>>(tcount, (long long)tiles, flop_tile);
+  note_launch(4);
   e = cudaGetLastError();
+  cudaFreeAsync(tile_keys, st);
+  cudaFreeAsync(tlist, st);
+  cudaFreeAsync(reg_keys, st);
   cudaFreeAsync(dgr, st);
+  return e;
+}
+
+cudaError_t gemm_flops(unsigned long long* value, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(value, g_gemm_flops, sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long zero = 0;
+    e = cudaMemcpyToSymbol(g_gemm_flops, &zero, sizeof(zero));
+  }
   return e;
 }
 

@@ -504,3 +504,30 @@ def test_batched_large_k_two_fields_and_dense(k):
     assert np.max(np.abs(got - ref)) <= KSG_TOL
     fa.close()
     fb.close()
+
+
+def test_pearson_screen_many_near_max_tiles():
+    """The exhaustive Pearson path screens tiles with the hi*hi product and runs the exact split-TF32
+    product only where a tile can hold the region pair's maximum.  Here every series is one shared
+    signal plus small noise (|r| ~ 0.999 everywhere), so nearly all tiles lie within the screening
+    margin and pass 2 runs on a long tile list; half of the B points carry the negated signal
+    (CORR_F_ABS), and two B points duplicate A points exactly (r = 1 up to rounding)."""
+    n, nx, ny, nz = 100, 64, 32, 4
+    g = torch.Generator().manual_seed(21)
+    sig = torch.randn(n, 1, generator=g, dtype=torch.float64)
+    noise = torch.randn(n, nx * ny * nz, generator=g, dtype=torch.float64)
+    vals = (sig + 0.03 * noise).to(torch.float32)
+    vals[:, nx // 2 + 8::nx] *= -1  # a column of B with the negated signal
+    p_a1, p_a2 = 5 * nx + 3, 17 * nx + 30                     # in A = x < 32
+    p_b1, p_b2 = 9 * nx + 40, 2 * nx * ny + 20 * nx + 50     # in B = x >= 32
+    vals[:, p_b1] = vals[:, p_a1]
+    vals[:, p_b2] = vals[:, p_a2]
+    f = cb.corr_field_create(vals.cuda(), nx, ny, nz, n)
+    host = vals.numpy()
+    A, B = [(0, 0, 0, 32, ny, nz)], [(32, 0, 0, nx, ny, nz)]
+    _block_compare(f, None, host, None, (nx, ny, nz), A, B)
+    _block_compare(f, None, host, None, (nx, ny, nz), A, B, absval=True)
+    m, a = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, A, B, 0, 0)
+    # the two duplicated series give r = 1 up to the split-TF32 rounding (~1e-6): one of them wins
+    assert abs(float(m[0]) - 1.0) <= PEARSON_TOL and tuple(_cpu(a)[0]) in ((p_a1, p_b1), (p_a2, p_b2))
+    f.close()
