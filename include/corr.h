@@ -154,11 +154,11 @@ int corr_check(const corr_field* f, void* cuda_stream);
 int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset);
 
 /* corr_gemm_flops -- tensor-core work executed on `device` by the exhaustive Pearson block path
- * (corr_region_max with samples == 0) since the last reset: logical MMA flops 2*128*256*K per
- * 128x256 tile and MMA pass (the screening pass runs 1 tf32 MMA set per tile, the exact pass 3 on the
- * tiles that can hold a region pair's maximum).  Synchronises the device; reset != 0 zeroes it.
- * Diagnostic for the roofline report (bench.py). */
-int corr_gemm_flops(int32_t device, int64_t* flops, int32_t reset);
+ * (corr_region_max with samples == 0) since the last reset, as logical MMA flops 2*128*256*K per
+ * 128x256 tile and MMA set: *bf16_flops for the screening pass (one bf16 product per tile),
+ * *tf32_flops for the exact pass (three tf32 products on the tiles that can hold a region pair's
+ * maximum).  Synchronises the device; reset != 0 zeroes both.  Diagnostic for bench.py's roofline. */
+int corr_gemm_flops(int32_t device, int64_t* bf16_flops, int64_t* tf32_flops, int32_t reset);
 
 /* Number of CUDA kernels this library has launched in this process (diagnostic; bench.py
  * reports the launches inside its timed region as `gpu_launches`). */

@@ -66,7 +66,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     L.corr_check.argtypes = [vp, vp]
     L.corr_launch_count.argtypes = []
     L.corr_ksg_comparisons.argtypes = [i32, ctypes.POINTER(i64), i32]
-    L.corr_gemm_flops.argtypes = [i32, ctypes.POINTER(i64), i32]
+    L.corr_gemm_flops.argtypes = [i32, ctypes.POINTER(i64), ctypes.POINTER(i64), i32]
     L.corr_last_error.restype = ctypes.c_char_p
     L.corr_last_error.argtypes = []
     for name in EXPORTS[:-2]:
@@ -228,10 +228,11 @@ def corr_ksg_comparisons(device: int = 0, reset: bool = True) -> int:
     return v.value
 
 
-def corr_gemm_flops(device: int = 0, reset: bool = True) -> int:
-    v = ctypes.c_int64()
-    _check(load().corr_gemm_flops(device, ctypes.byref(v), int(reset)))
-    return v.value
+def corr_gemm_flops(device: int = 0, reset: bool = True) -> Tuple[int, int]:
+    """(bf16 screening-pass flops, tf32 exact-pass flops) since the last reset."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().corr_gemm_flops(device, ctypes.byref(a), ctypes.byref(b), int(reset)))
+    return a.value, b.value
 
 
 def corr_launch_count() -> int:

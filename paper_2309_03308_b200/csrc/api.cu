@@ -52,6 +52,7 @@ void free_field(corr_field* f) {
   cudaFree(f->Z);
   cudaFree(f->Zhi);
   cudaFree(f->Zlo);
+  cudaFree(f->Zb);
   cudaFree(f->S);
   cudaFree(f->perm);
   cudaFree(f->cflag);
@@ -97,6 +98,7 @@ int alloc_field(int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t dev
   };
   if (!alloc((void**)&f->F, row_elems * 4) || !alloc((void**)&f->Z, row_elems * 4) ||
       !alloc((void**)&f->Zhi, row_elems * 4) || !alloc((void**)&f->Zlo, row_elems * 4) ||
+      !alloc((void**)&f->Zb, row_elems * 2) ||
       !alloc((void**)&f->S, row_elems * 4) || !alloc((void**)&f->perm, row_elems * 2) ||
       !alloc((void**)&f->cflag, (size_t)f->P) || !alloc((void**)&f->spread, (size_t)f->P * 4) ||
       !alloc((void**)&f->psi, ((size_t)members + 2) * 8) || !alloc((void**)&f->err, 2 * sizeof(int))) {
@@ -203,15 +205,16 @@ int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset) {
   return CORR_OK;
 }
 
-int corr_gemm_flops(int32_t device, int64_t* flops, int32_t reset) {
-  if (!flops) return fail(CORR_E_INVAL, "flops is NULL");
+int corr_gemm_flops(int32_t device, int64_t* bf16_flops, int64_t* tf32_flops, int32_t reset) {
+  if (!bf16_flops || !tf32_flops) return fail(CORR_E_INVAL, "output pointer is NULL");
   DeviceGuard guard(device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   cudaError_t e = cudaDeviceSynchronize();
-  unsigned long long v = 0;
-  if (e == cudaSuccess) e = gemm_flops(&v, reset != 0);
+  unsigned long long v[2] = {0, 0};
+  if (e == cudaSuccess) e = gemm_flops(v, reset != 0);
   if (e != cudaSuccess) return cuda_fail(e, "corr_gemm_flops");
-  *flops = (int64_t)v;
+  *bf16_flops = (int64_t)v[0];
+  *tf32_flops = (int64_t)v[1];
   return CORR_OK;
 }
 

@@ -18,6 +18,7 @@ struct corr_field {
   float* Z;       // [P][n_pad] (x - mean)/||x - mean|| (fp64 -> fp32), pad = 0
   float* Zhi;     // [P][n_pad] tf32(Z)               (split-TF32 high part)
   float* Zlo;     // [P][n_pad] tf32(Z - Zhi)         (split-TF32 low part)
+  uint16_t* Zb;   // [P][n_pad] bf16(Z)  (screening pass of the exhaustive Pearson GEMM)
   float* S;       // [P][n_pad] row sorted ascending, pad = +inf
   uint16_t* perm; // [P][n_pad] argsort of the row (S[p][t] = F[p][perm[p][t]])
   uint8_t* cflag; // [P] 1 = constant series (min == max)
@@ -75,7 +76,7 @@ cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int f
 cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1,
                        const PairSrc& src, const PairOut& out, cudaStream_t st);
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset);
-cudaError_t gemm_flops(unsigned long long* value, bool reset);
+cudaError_t gemm_flops(unsigned long long* value /* [2]: bf16, tf32 */, bool reset);
 cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
                                  const PairOut& out, cudaStream_t st);
 cudaError_t launch_region_finalize(const PairSrc& src, const unsigned long long* keys,

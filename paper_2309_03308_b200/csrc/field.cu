@@ -13,6 +13,8 @@
 // All kernels are HBM-bound; DESIGN.md lists their algorithmic bytes.
 #include <math.h>
 
+#include <cuda_bf16.h>
+
 #include <cub/block/block_radix_sort.cuh>
 
 #include "corr_internal.cuh"
@@ -64,6 +66,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // ---- 2. per-point statistics, standardisation, tf32 split (one warp per row) ---
 __global__ void __launch_bounds__(256) stats_kernel(const float* __restrict__ F, float* __restrict__ Z,
                                                     float* __restrict__ Zhi, float* __restrict__ Zlo,
+                                                    uint16_t* __restrict__ Zb,
                                                     uint8_t* __restrict__ cflag, float* __restrict__ spread,
                                                     int n, int n_pad, int64_t P) {
   const int lane = threadIdx.x & 31;
@@ -101,6 +104,7 @@ __global__ void __launch_bounds__(256) stats_kernel(const float* __restrict__ F,
     Z[p * n_pad + e] = z;
     Zhi[p * n_pad + e] = hi;
     Zlo[p * n_pad + e] = lo;
+    Zb[p * n_pad + e] = __bfloat16_as_ushort(__float2bfloat16_rn(z));
   }
   if (lane == 0) {
     cflag[p] = constant ? 1 : 0;
@@ -285,7 +289,7 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
   }
   {
     const int64_t threads = P * 32;
-    stats_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(f->F, f->Z, f->Zhi, f->Zlo, f->cflag,
+    stats_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(f->F, f->Z, f->Zhi, f->Zlo, f->Zb, f->cflag,
                                                                    f->spread, f->n, f->n_pad, P);
   }
   {

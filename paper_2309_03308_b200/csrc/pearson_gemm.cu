@@ -103,6 +103,14 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uin
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
+__device__ __forceinline__ void tc_mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
 // K-major operand, 128-byte swizzle atoms of 8 rows x 128 B (SBO = 1024 B), sm_100 version 1
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -113,6 +121,8 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 }
 // instruction descriptor: D=f32, A=B=tf32, K-major both, N=256, M=128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// D=f32, A=B=bf16 (kind::f16), K-major both, N=256, M=128 -- the screening pass
+constexpr uint32_t kIdescBF16 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -168,7 +178,9 @@ __device__ __forceinline__ float unord32(uint32_t u) {
 // records each tile's masked maximum (tile_keys[t]) and each region pair's (reg_keys[r]).
 // SCREEN = false: the full split-TF32 product with the max/argmax epilogue, over the tile list
 // tlist[0 .. *tcount) (or every tile when tlist == nullptr).
-template <bool SCREEN>
+// SCREEN with BF16: the screening maps are bf16 planes (64 members per 128-byte k-block row, one
+// kind::f16 MMA per 16 members) -- twice the members per k-block, half the operand bytes.
+template <bool SCREEN, bool BF16 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     pearson_block_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                          const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
@@ -230,9 +242,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(empty + s, ph ^ 1);
           unsigned char* st = stage_base + s * STAGE_BYTES;
           mbar_expect_tx(full + s, SCREEN ? A_BYTES + B_BYTES : STAGE_BYTES);
-          tma_load_4d(st, &mAhi, full + s, kb * BK, ax, ay, az);
+          const int k0 = kb * (BF16 ? 2 * BK : BK);  // members per k-block: 32 tf32 or 64 bf16 (128 B)
+          tma_load_4d(st, &mAhi, full + s, k0, ax, ay, az);
           if (!SCREEN) tma_load_4d(st + A_BYTES, &mAlo, full + s, kb * BK, ax, ay, az);
-          tma_load_4d(st + 2 * A_BYTES, &mBhi, full + s, kb * BK, bx, by, bz);
+          tma_load_4d(st + 2 * A_BYTES, &mBhi, full + s, k0, bx, by, bz);
           if (!SCREEN) tma_load_4d(st + 2 * A_BYTES + B_BYTES, &mBlo, full + s, kb * BK, bx, by, bz);
         }
       }
@@ -257,7 +270,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 bytes inside the swizzle atom
             const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
-            tc_mma_tf32(dcol, dAhi + adv, dBhi + adv, kIdesc, first);
+            if (BF16) tc_mma_bf16(dcol, dAhi + adv, dBhi + adv, kIdescBF16, first);
+            else tc_mma_tf32(dcol, dAhi + adv, dBhi + adv, kIdesc, first);
             if (!SCREEN) {
               tc_mma_tf32(dcol, dAhi + adv, dBlo + adv, kIdesc, 1u);
               tc_mma_tf32(dcol, dAlo + adv, dBhi + adv, kIdesc, 1u);
@@ -725,6 +739,20 @@ bool make_map(CUtensorMap* m, const float* plane, const corr_field* f, int bx, i
   return r == CUDA_SUCCESS;
 }
 
+bool make_map_bf16(CUtensorMap* m, const uint16_t* plane, const corr_field* f, int bx, int by, int bz) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)f->n_pad, (cuuint64_t)f->nx, (cuuint64_t)f->ny, (cuuint64_t)f->nz};
+  cuuint64_t strides[3] = {(cuuint64_t)f->n_pad * 2, (cuuint64_t)f->n_pad * 2 * f->nx,
+                           (cuuint64_t)f->n_pad * 2 * f->nx * f->ny};
+  cuuint32_t box[4] = {(cuuint32_t)(2 * BK), (cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)plane, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int pow2ceil(int v) {
   int p = 1;
   while (p < v) p <<= 1;
@@ -811,11 +839,14 @@ cudaError_t launch_pearson_block2(const corr_field* fa, const corr_field* fb, co
 
 // executed tensor-core work of the block GEMMs (logical MMA flops incl. tile padding): the
 // roofline numerator of bench.py's Pearson block line (corr_gemm_flops)
-__device__ unsigned long long g_gemm_flops;
+// [0]: bf16 flops (the screening pass), [1]: tf32 flops (the exact pass; a tf32 screen too)
+__device__ unsigned long long g_gemm_flops[2];
 
-__global__ void gemm_account_kernel(const int* __restrict__ tcount, long long tiles_screen, long long flop_per_mma_tile) {
-  const long long exact = tcount ? (long long)*tcount : 0;
-  atomicAdd(&g_gemm_flops, (unsigned long long)((tiles_screen + 3 * exact) * flop_per_mma_tile));
+__global__ void gemm_account_kernel(const int* __restrict__ tcount, long long tiles_screen, long long flop_per_mma_tile,
+                                    int screen_bf16, long long tiles_exact_all) {
+  const long long exact = tcount ? (long long)*tcount : tiles_exact_all;
+  atomicAdd(&g_gemm_flops[screen_bf16 ? 0 : 1], (unsigned long long)(tiles_screen * flop_per_mma_tile));
+  atomicAdd(&g_gemm_flops[1], (unsigned long long)(3 * exact * flop_per_mma_tile));
 }
 
 // screen -> tile list: keep tile t iff its approximate maximum is within delta of its region pair's
@@ -903,6 +934,8 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   e = cudaFuncSetAttribute(pearson_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(pearson_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(pearson_block_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = kSMs;
   cudaGetDevice(&dev);
@@ -916,7 +949,7 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   if (noscreen || tiles >= (int64_t)INT32_MAX) {
     pearson_block_kernel<false><<<(unsigned)grid, kThreads, smem, st>>>(
         mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag, keys, nullptr, nullptr, nullptr, nullptr);
-    gemm_account_kernel<<<1, 1, 0, st>>>(nullptr, 3LL * tiles, flop_tile);
+    gemm_account_kernel<<<1, 1, 0, st>>>(nullptr, 0, flop_tile, 0, (long long)tiles);
     note_launch(2);
     e = cudaGetLastError();
     cudaFreeAsync(dgr, st);
@@ -932,9 +965,23 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   //                 truncating adds) -> 2 * K * 2^-23 for both passes together
   // A tile whose approximate maximum is below (region approx max - 2b) holds only entries whose
   // exact value is below the region's maximum, so dropping it changes neither max nor argmax.
-  const double b_bound = 2.0 * std::ldexp(1.0, -11) + std::ldexp(1.0, -22) +
-                         2.0 * (double)(g.kblocks * BK) * std::ldexp(1.0, -23) + 1e-6;
-  const float delta = (float)(2.0 * b_bound * 1.1);  // 10 % margin; 2.7e-3 at n = 1000
+  // The screening pass runs on bf16(Z) (unit roundoff 2^-8) unless CORR_GEMM_SCREEN_TF32=1 selects
+  // tf32 Z_hi (2^-11): bf16 moves half the operand bytes and runs the MMA at twice the rate, at
+  // the price of a wider margin (1.8e-2 vs 2.7e-3 at n = 1000), i.e. a few more kept tiles.
+  static const int screen_tf32 = [] {
+    const char* v = getenv("CORR_GEMM_SCREEN_TF32");
+    return (v && v[0] == '1') ? 1 : 0;
+  }();
+  const double u_scr = screen_tf32 ? std::ldexp(1.0, -11) : std::ldexp(1.0, -8);
+  const double b_bound = 2.0 * u_scr + u_scr * u_scr + 2.0 * (double)(g.kblocks * BK) * std::ldexp(1.0, -23) + 1e-6;
+  const float delta = (float)(2.0 * b_bound * 1.1);  // 10 % margin
+  GemmGeom gs = g;  // the bf16 screen covers 64 members per k-block
+  CUtensorMap mAb, mBb;
+  if (!screen_tf32) {
+    gs.kblocks = (fa->n_pad + 2 * BK - 1) / (2 * BK);
+    if (!make_map_bf16(&mAb, fa->Zb, fa, g.bxA, g.byA, g.bzA) || !make_map_bf16(&mBb, fb->Zb, fb, g.bxB, g.byB, g.bzB))
+      return cudaErrorNotSupported;
+  }
   uint32_t* tile_keys = nullptr;
   uint32_t* reg_keys = nullptr;
   int* tlist = nullptr;
@@ -946,13 +993,19 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   tcount = reinterpret_cast<int*>(reg_keys + nreg);
   cudaMemsetAsync(tile_keys, 0, (size_t)tiles * 4, st);
   cudaMemsetAsync(reg_keys, 0, (size_t)nreg * 4 + 16, st);
-  pearson_block_kernel<true><<<(unsigned)grid, kThreads, smem, st>>>(
-      mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag, keys, nullptr, nullptr, tile_keys, reg_keys);
+  if (screen_tf32)
+    pearson_block_kernel<true><<<(unsigned)grid, kThreads, smem, st>>>(
+        mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag, keys, nullptr, nullptr, tile_keys, reg_keys);
+  else
+    pearson_block_kernel<true, true><<<(unsigned)grid, kThreads, smem, st>>>(
+        mAb, mAb, mBb, mBb, dgr, gs, fa->cflag, fb->cflag, keys, nullptr, nullptr, tile_keys, reg_keys);
   screen_select_kernel<<<(unsigned)std::min<int64_t>((tiles + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(
       dgr, g.nreg, tiles, tile_keys, reg_keys, tlist, tcount, delta);
   pearson_block_kernel<false><<<(unsigned)grid, kThreads, smem, st>>>(
       mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag, keys, tlist, tcount, nullptr, nullptr);
-  gemm_account_kernel<<<1, 1, 0, st>>>(tcount, (long long)tiles, flop_tile);
+  // executed work: the screen's MMA count per tile equals one tf32 set (same K coverage), counted
+  // as one set of 2*M*N*K flops (bf16 or tf32)
+  gemm_account_kernel<<<1, 1, 0, st>>>(tcount, (long long)tiles, flop_tile, screen_tf32 ? 0 : 1, 0);
   note_launch(4);
   e = cudaGetLastError();
   cudaFreeAsync(tile_keys, st);
@@ -963,10 +1016,10 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
 }
 
 cudaError_t gemm_flops(unsigned long long* value, bool reset) {
-  cudaError_t e = cudaMemcpyFromSymbol(value, g_gemm_flops, sizeof(unsigned long long));
+  cudaError_t e = cudaMemcpyFromSymbol(value, g_gemm_flops, 2 * sizeof(unsigned long long));
   if (e == cudaSuccess && reset) {
-    const unsigned long long zero = 0;
-    e = cudaMemcpyToSymbol(g_gemm_flops, &zero, sizeof(zero));
+    const unsigned long long zero[2] = {0, 0};
+    e = cudaMemcpyToSymbol(g_gemm_flops, zero, sizeof(zero));
   }
   return e;
 }

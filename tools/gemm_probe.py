@@ -35,7 +35,7 @@ for cfg in (synth.C2, synth.C4):
         A, B = cb.boxes(A), cb.boxes(B)
         cb.corr_gemm_flops(0, reset=True)
         dt = timed(lambda: cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, A, B, 0, 0))
-        exe = cb.corr_gemm_flops(0, reset=True) / 4  # timed() runs the call 1 + 3 times
+        exe = sum(cb.corr_gemm_flops(0, reset=True)) / 4  # timed() runs the call 1 + 3 times
         pairs = sum((b.x1 - b.x0) * (b.y1 - b.y0) * (b.z1 - b.z0) * (a.x1 - a.x0) * (a.y1 - a.y0) * (a.z1 - a.z0)
                     for a, b in zip(A, B))
         res[f"{cfg.name}_{name}"] = {"s": dt, "pairs_per_s": pairs / dt,
