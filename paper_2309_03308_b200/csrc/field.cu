@@ -8,6 +8,7 @@
 //   Z  [P][n_pad]  standardised series (x - mean)/||x - mean||, fp64 -> fp32
 //                  (Pearson = <Z_a, Z_b>, "means and variances")
 //   Zhi, Zlo       split-TF32 planes: Zhi = tf32_rna(Z), Zlo = tf32_rna(Z - Zhi)
+//   Zb             bf16_rn(Z): the screening pass of the exhaustive Pearson GEMM
 //   S, perm        row sorted ascending (+inf pad) and its argsort (uint16)
 //   cflag          constant series (min == max) -> NaN correlations (reading R10)
 // All kernels are HBM-bound; DESIGN.md lists their algorithmic bytes.
