@@ -389,9 +389,12 @@ def main():
                       "cublas_tf32_measured": tf32_ctx,
                       "pairs_per_s": nA * nB / (stage_ms["pearson_block"] / 1e3),
                       "ms_per_step": stage_ms["pearson_block"]}
-    ps_gbs = my_pairs * (8 * spec.n_pad if hasattr(spec, "n_pad") else 8 * ((n + 7) // 8 * 8)) / (
-        stage_ms["pearson_sampled"] / 1e3) / 1e9
-    roofline_pearson_pairs = {"bound": "hbm", "kernel": "pearson_pairs_kernel", "achieved": ps_gbs,
+    # screened sampled Pearson: a bf16 pass over every pair (2 rows x n_pad x 2 B + the per-pair
+    # approximate value, 4 B written and read back) and an fp32 pass over the few candidates
+    n_pad = (n + 7) // 8 * 8
+    ps_gbs = my_pairs * (4 * n_pad + 8) / (stage_ms["pearson_sampled"] / 1e3) / 1e9
+    roofline_pearson_pairs = {"bound": "hbm", "kernel": "pearson_screen_kernel (bf16) + pearson_exact_selected_kernel",
+                              "bytes_per_pair": 4 * n_pad + 8, "achieved": ps_gbs,
                               "peak": peaks.get("hbm_gbs") or 6552.3, "unit": "GB/s",
                               "frac": ps_gbs / (peaks.get("hbm_gbs") or 6552.3),
                               "pairs_per_s": my_pairs / (stage_ms["pearson_sampled"] / 1e3),
