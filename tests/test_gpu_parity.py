@@ -531,3 +531,19 @@ def test_pearson_screen_many_near_max_tiles():
     # the two duplicated series give r = 1 up to the split-TF32 rounding (~1e-6): one of them wins
     assert abs(float(m[0]) - 1.0) <= PEARSON_TOL and tuple(_cpu(a)[0]) in ((p_a1, p_b1), (p_a2, p_b2))
     f.close()
+
+
+@pytest.mark.parametrize("n", [100, 1000])
+def test_batch_equals_single_calls(n):
+    """a batch of point pairs gives bit-for-bit the results of one call per pair
+    (pairs are independent units; the sampler and the schedule never mix them)."""
+    spec = synth.field_spec(8, 8, 2, n, seed=31 + n)
+    vals, f = _field(spec)
+    a, b = synth.random_pairs(spec.points, 24, seed=n)
+    ta, tb = a.cuda(), b.cuda()
+    for measure in (cb.CORR_KSG, cb.CORR_PEARSON, cb.CORR_KSG | cb.CORR_F_KSG_PLUS1):
+        batch = _cpu(cb.corr_eval_pairs(f, None, measure, 3, ta, tb))
+        single = np.concatenate([_cpu(cb.corr_eval_pairs(f, None, measure, 3, ta[i:i + 1], tb[i:i + 1]))
+                                 for i in range(len(a))])
+        assert np.array_equal(batch, single, equal_nan=True), measure
+    f.close()
