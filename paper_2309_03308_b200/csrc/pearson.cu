@@ -227,7 +227,10 @@ cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, con
     uint32_t* regkey = nullptr;
     cudaError_t e = cudaMallocAsync((void**)&approx, (size_t)src.nunits * 4, st);
     if (e == cudaSuccess) e = cudaMallocAsync((void**)&regkey, (size_t)src.nreg * 4, st);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+      if (approx) cudaFreeAsync(approx, st);
+      return e;
+    }
     cudaMemsetAsync(regkey, 0, (size_t)src.nreg * 4, st);
     const double uu = 1.0 / 256.0;  // bf16 unit roundoff 2^-8
     const double b_bound = 2.0 * uu + uu * uu + 2.0 * (double)fa->n_pad / 8388608.0 + 1e-6;

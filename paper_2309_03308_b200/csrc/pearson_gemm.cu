@@ -979,8 +979,10 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   CUtensorMap mAb, mBb;
   if (!screen_tf32) {
     gs.kblocks = (fa->n_pad + 2 * BK - 1) / (2 * BK);
-    if (!make_map_bf16(&mAb, fa->Zb, fa, g.bxA, g.byA, g.bzA) || !make_map_bf16(&mBb, fb->Zb, fb, g.bxB, g.byB, g.bzB))
+    if (!make_map_bf16(&mAb, fa->Zb, fa, g.bxA, g.byA, g.bzA) || !make_map_bf16(&mBb, fb->Zb, fb, g.bxB, g.byB, g.bzB)) {
+      cudaFreeAsync(dgr, st);
       return cudaErrorNotSupported;
+    }
   }
   uint32_t* tile_keys = nullptr;
   uint32_t* reg_keys = nullptr;
@@ -989,7 +991,12 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   e = cudaMallocAsync((void**)&tile_keys, (size_t)tiles * 4, st);
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&tlist, (size_t)tiles * 4, st);
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&reg_keys, (size_t)nreg * 4 + 16, st);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    if (tile_keys) cudaFreeAsync(tile_keys, st);
+    if (tlist) cudaFreeAsync(tlist, st);
+    cudaFreeAsync(dgr, st);
+    return e;
+  }
   tcount = reinterpret_cast<int*>(reg_keys + nreg);
   cudaMemsetAsync(tile_keys, 0, (size_t)tiles * 4, st);
   cudaMemsetAsync(reg_keys, 0, (size_t)nreg * 4 + 16, st);
