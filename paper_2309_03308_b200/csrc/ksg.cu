@@ -628,7 +628,7 @@ __device__ __forceinline__ int ksg_block_big(const float2* __restrict__ xy, cons
 }
 
 template <int K, int RM, int G, bool SWEEP>
-__global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? 8 : 3))) ksg_sorted_kernel(
+__global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? (K <= 4 ? 10 : 9) : 3))) ksg_sorted_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Fa,
     const float* __restrict__ Sb, const uint16_t* __restrict__ Pb, const float* __restrict__ Fb,
     const float* __restrict__ spa, const float* __restrict__ spb, const uint8_t* __restrict__ ca,
