@@ -430,6 +430,9 @@ __device__ __forceinline__ int ksg_block(const float2* __restrict__ xy, const fl
           if constexpr (PARTIAL && RM == 1 && K <= 8) chunk_adjacent<K, true>(xy4 + hlo * 16, zi, l);
           else chunk_plain<K, RM>(xy4 + hlo * 16, zi, l, 32);
         }
+        // warp kernel (n < 128): the compact filtered loop -- its code path runs on few chunks per
+        // pair, and the unrolled body costs more in i-cache misses than it saves (C3 +4 %)
+        else if constexpr (PARTIAL) chunk_filtered_rm<K, RM, G, true>(xy4 + hlo * 16, zi, l, 32);
         else chunk_filtered<K, RM, G, true>(xy4 + hlo * 16, zi, l, 32);
         ncand += 32;
         --hlo;
@@ -456,7 +459,8 @@ __device__ __forceinline__ int ksg_block(const float2* __restrict__ xy, const fl
             chunk_plain<K, RM>(xy4 + hhi * 16, zi, l, PARTIAL ? cnt : 32);
           }
         }
-        else chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l, PARTIAL ? cnt : 32);
+        else if constexpr (PARTIAL) chunk_filtered_rm<K, RM, G, false>(xy4 + hhi * 16, zi, l, cnt);
+        else chunk_filtered<K, RM, G, false>(xy4 + hhi * 16, zi, l, 32);
         ncand += cnt;
         ++hhi;
       }
