@@ -460,9 +460,12 @@ def main():
         # at least 6 steps: the first step's upload + ingest is the pipeline fill (not overlapped),
         # later uploads overlap the previous step's compute
         ne = max(6, args.steps)
+        e2e_clocks = ClockSampler(local)
+        e2e_clocks.start()
         te = time.perf_counter()
         run_e2e(ne)
         e_s = (time.perf_counter() - te) / ne
+        e2e_clk = e2e_clocks.stop()
         if world > 1:
             tt = torch.tensor([e_s], dtype=torch.float64, device=f"cuda:{local}")
             tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
@@ -473,6 +476,7 @@ def main():
         e2e = {"value": total_pairs / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h_holder[0], "s_per_step": e_s,
                "device_step_ms": [round(a.elapsed_time(b), 1) for a, b in step_evs],
+               "clocks": e2e_clk,
                "includes": "per step: pinned-host upload of the 7.04 GB field (1/N of the member rows per "
                             "rank, exchanged by NCCL broadcasts), "
                            "corr_field_update ingest, the step, D2H of the maxima; double-buffered "

@@ -2,6 +2,7 @@
 upload (H2D + corr_field_update on a side stream) and of the step (KSG + Pearson region max) on
 the compute stream, for the double-buffered bench.py e2e loop at C4 (1 GPU)."""
 import json
+import os
 import sys
 import time
 
@@ -43,10 +44,12 @@ def upload(slot, after=None):
         if after is not None:
             up.wait_event(after)
         e0 = ev(up)
-        bufs[slot].copy_(host, non_blocking=True)
+        if not os.environ.get("E2E_NO_H2D"):  # diagnostics: which half of the upload slows the step
+            bufs[slot].copy_(host, non_blocking=True)
         e1 = ev(up)
         t = time.perf_counter()
-        cb.corr_field_update(slots[slot], bufs[slot], stream=up)
+        if not os.environ.get("E2E_NO_UPDATE"):
+            cb.corr_field_update(slots[slot], bufs[slot], stream=up)
         th = time.perf_counter() - t
         e2 = ev(up)
     return e0, e1, e2, th
