@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "sampler.cuh"
@@ -204,6 +205,54 @@ int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset) {
   *count = (int64_t)v;
   return CORR_OK;
 }
+
+}  // extern "C"
+
+namespace corr {
+namespace {
+struct TableEntry {
+  int device;
+  uint64_t hash;
+  std::vector<unsigned char> bytes;
+  void* dptr;
+};
+std::mutex g_table_mu;
+std::vector<TableEntry> g_tables;
+size_t g_table_bytes = 0;
+constexpr size_t kTableCacheBytes = 256u << 20;
+uint64_t fnv1a(const unsigned char* p, size_t n) {
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
+  return h;
+}
+}  // namespace
+
+const void* cached_table(int device, const void* host, size_t bytes, cudaStream_t st) {
+  const unsigned char* hp = static_cast<const unsigned char*>(host);
+  const uint64_t h = fnv1a(hp, bytes);
+  std::lock_guard<std::mutex> lock(g_table_mu);
+  for (const TableEntry& t : g_tables)
+    if (t.device == device && t.hash == h && t.bytes.size() == bytes && memcmp(t.bytes.data(), hp, bytes) == 0)
+      return t.dptr;
+  if (g_table_bytes + bytes > kTableCacheBytes) return nullptr;  // caller falls back to a per-call copy
+  void* d = nullptr;
+  if (cudaMalloc(&d, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  // first use: ordered on the caller's stream (tables are immutable afterwards)
+  if (cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  g_tables.push_back(TableEntry{device, h, std::vector<unsigned char>(hp, hp + bytes), d});
+  g_table_bytes += bytes;
+  return d;
+}
+}  // namespace corr
+
+extern "C" {
 
 int corr_gemm_flops(int32_t device, int64_t* bf16_flops, int64_t* tf32_flops, int32_t reset) {
   if (!bf16_flops || !tf32_flops) return fail(CORR_E_INVAL, "output pointer is NULL");
@@ -404,10 +453,15 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
   cudaStream_t st = (cudaStream_t)cuda_stream;
   RegionDev* dreg = nullptr;
   unsigned long long* keys = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&dreg, reg.size() * sizeof(RegionDev), st);
+  // the region table: resident device copy reused across calls with the same regions (context view)
+  const size_t reg_bytes = reg.size() * sizeof(RegionDev);
+  dreg = const_cast<RegionDev*>(static_cast<const RegionDev*>(cached_table(fa->device, reg.data(), reg_bytes, st)));
+  const bool own_reg = dreg == nullptr;
+  cudaError_t e = cudaSuccess;
+  if (own_reg) e = cudaMallocAsync((void**)&dreg, reg_bytes, st);
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&keys, (size_t)nregion_pairs * 8, st);
   if (e != cudaSuccess) return cuda_fail(e, "corr_region_max alloc");
-  e = cudaMemcpyAsync(dreg, reg.data(), reg.size() * sizeof(RegionDev), cudaMemcpyHostToDevice, st);
+  if (own_reg) e = cudaMemcpyAsync(dreg, reg.data(), reg_bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(keys, 0, (size_t)nregion_pairs * 8, st);
 
   PairSrc src;
@@ -430,7 +484,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
     if ((measure & 0xFF) == CORR_KSG) {
       e = launch_ksg(fa, fb, k, ksg_flags(measure), src, po, st);
       if (e == cudaErrorNotSupported) {
-        cudaFreeAsync(dreg, st);
+        if (own_reg) cudaFreeAsync(dreg, st);
         cudaFreeAsync(keys, st);
         return fail(CORR_E_INVAL, "KSG with k > 32 is not supported");
       }
@@ -445,7 +499,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
     }
   }
   if (e == cudaSuccess) e = launch_region_finalize(src, keys, out_max, out_argmax, st);
-  cudaFreeAsync(dreg, st);
+  if (own_reg) cudaFreeAsync(dreg, st);
   cudaFreeAsync(keys, st);
   if (e != cudaSuccess) return cuda_fail(e, "corr_region_max");
   return CORR_OK;

@@ -76,6 +76,11 @@ cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int f
 cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1,
                        const PairSrc& src, const PairOut& out, cudaStream_t st);
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset);
+// Device copy of a small host table (region lists) that stays resident and is reused when the
+// same bytes come again: no host->device copy on the call path of repeated calls.  (A small copy
+// queued behind a large pinned upload on the same copy engine would otherwise stall the stream
+// for the whole upload.)  Returns nullptr on failure.
+const void* cached_table(int device, const void* host, size_t bytes, cudaStream_t st);
 cudaError_t gemm_flops(unsigned long long* value /* [2]: bf16, tf32 */, bool reset);
 cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
                                  const PairOut& out, cudaStream_t st);

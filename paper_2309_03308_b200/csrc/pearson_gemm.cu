@@ -925,11 +925,17 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   if (!make_map(&mAhi, fa->Zhi, fa, g.bxA, g.byA, g.bzA) || !make_map(&mAlo, fa->Zlo, fa, g.bxA, g.byA, g.bzA) ||
       !make_map(&mBhi, fb->Zhi, fb, g.bxB, g.byB, g.bzB) || !make_map(&mBlo, fb->Zlo, fb, g.bxB, g.byB, g.bzB))
     return cudaErrorNotSupported;
-  GemmRegion* dgr = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&dgr, gr.size() * sizeof(GemmRegion), st);
-  if (e != cudaSuccess) return e;
-  e = cudaMemcpyAsync(dgr, gr.data(), gr.size() * sizeof(GemmRegion), cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return e;
+  // the tile table: resident device copy reused across calls with the same region pairs
+  GemmRegion* dgr = const_cast<GemmRegion*>(
+      static_cast<const GemmRegion*>(cached_table(fa->device, gr.data(), gr.size() * sizeof(GemmRegion), st)));
+  const bool own_gr = dgr == nullptr;
+  cudaError_t e = cudaSuccess;
+  if (own_gr) {
+    e = cudaMallocAsync((void**)&dgr, gr.size() * sizeof(GemmRegion), st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(dgr, gr.data(), gr.size() * sizeof(GemmRegion), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+  }
   const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16 + 2 * BN * 4 + 2 * BN * 4;
   e = cudaFuncSetAttribute(pearson_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
@@ -952,7 +958,7 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
     gemm_account_kernel<<<1, 1, 0, st>>>(nullptr, 0, flop_tile, 0, (long long)tiles);
     note_launch(2);
     e = cudaGetLastError();
-    cudaFreeAsync(dgr, st);
+    if (own_gr) cudaFreeAsync(dgr, st);
     return e;
   }
   // Screened two-pass evaluation (exact): pass 1 computes every tile with the hi*hi product only
@@ -980,7 +986,7 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   if (!screen_tf32) {
     gs.kblocks = (fa->n_pad + 2 * BK - 1) / (2 * BK);
     if (!make_map_bf16(&mAb, fa->Zb, fa, g.bxA, g.byA, g.bzA) || !make_map_bf16(&mBb, fb->Zb, fb, g.bxB, g.byB, g.bzB)) {
-      cudaFreeAsync(dgr, st);
+      if (own_gr) cudaFreeAsync(dgr, st);
       return cudaErrorNotSupported;
     }
   }
@@ -994,7 +1000,7 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   if (e != cudaSuccess) {
     if (tile_keys) cudaFreeAsync(tile_keys, st);
     if (tlist) cudaFreeAsync(tlist, st);
-    cudaFreeAsync(dgr, st);
+    if (own_gr) cudaFreeAsync(dgr, st);
     return e;
   }
   tcount = reinterpret_cast<int*>(reg_keys + nreg);
@@ -1018,7 +1024,7 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   cudaFreeAsync(tile_keys, st);
   cudaFreeAsync(tlist, st);
   cudaFreeAsync(reg_keys, st);
-  cudaFreeAsync(dgr, st);
+  if (own_gr) cudaFreeAsync(dgr, st);
   return e;
 }
 

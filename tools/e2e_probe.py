@@ -45,7 +45,9 @@ def upload(slot, after=None):
             up.wait_event(after)
         e0 = ev(up)
         if not os.environ.get("E2E_NO_H2D"):  # diagnostics: which half of the upload slows the step
-            bufs[slot].copy_(host, non_blocking=True)
+            frac = float(os.environ.get("E2E_H2D_FRAC", "1"))   # diagnostics: copy only part of the rows
+            m = max(1, int(round(frac * host.shape[0])))
+            bufs[slot][:m].copy_(host[:m], non_blocking=True)
         e1 = ev(up)
         t = time.perf_counter()
         if not os.environ.get("E2E_NO_UPDATE"):
