@@ -303,7 +303,7 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
       case 128: er = launch_sort_radix<32, 4>(f, st); break;
       case 256: er = launch_sort_radix<64, 4>(f, st); break;
       case 512: er = launch_sort_radix<64, 8>(f, st); break;
-      case 1024: er = launch_sort_radix<128, 8>(f, st); break;
+      case 1024: er = launch_sort_radix<64, 16>(f, st); break;
       case 2048: er = launch_sort_radix<256, 8>(f, st); break;
       case 4096: er = launch_sort_radix<256, 16>(f, st); break;
       default: break;
