@@ -1,6 +1,7 @@
 // Pipe-throughput microbenchmark for the KSG inner-loop instruction mix on sm_100a.
 // Measures warp-instructions issued per SM per cycle (clock64 per block) for
-// FMNMX, FMNMX3, FADD, FADD2, FFMA, IADD3, and mixes. Informs DESIGN.md's ALU roofline.
+// FMNMX, FMNMX3, FADD, FADD2, FFMA, IADD3, packed f16/bf16/s16 min-max, HADD2, HSETP2, F2FP, LOP3
+// and mixes. Informs DESIGN.md's ALU roofline.
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -55,6 +56,27 @@ __global__ void __launch_bounds__(256) bench(float* out, int iters, long long* c
         asm volatile("{.reg .pred q; setp.lt.f32 q, %0, %1; @q add.u32 %2, %2, 1;}" : "+f"(a[c]), "+f"(b[c]), "+r"(u[c]));
       }
       if (OP == 10) asm volatile("min.u32 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 1) % CH]));
+      if (OP == 12) {  // packed f16 min / max (alternating, as OP 0)
+        asm volatile("max.f16x2 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 1) % CH]));
+        asm volatile("min.f16x2 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 2) % CH]));
+      }
+      if (OP == 13) asm volatile("add.rn.f16x2 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 1) % CH]));
+      if (OP == 14) {  // packed f16 compare feeding a predicated add
+        asm volatile("{.reg .pred p, q; setp.lt.f16x2 p|q, %1, %2; @p add.u32 %0, %0, 1;}" : "+r"(u[c]) : "r"(u[(c + 1) % CH]), "r"(u[(c + 2) % CH]));
+      }
+      if (OP == 15) {  // f32 pair -> packed f16 (F2FP)
+        asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(u[c]) : "f"(a[c]), "f"(a[(c + 1) % CH]));
+        asm volatile("add.f32 %0, %0, 1.0;" : "+f"(a[c]));
+      }
+      if (OP == 16) {  // packed bf16 min / max
+        asm volatile("max.bf16x2 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 1) % CH]));
+        asm volatile("min.bf16x2 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 2) % CH]));
+      }
+      if (OP == 17) {  // packed s16 min / max
+        asm volatile("max.s16x2 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 1) % CH]));
+        asm volatile("min.s16x2 %0, %0, %1;" : "+r"(u[c]) : "r"(u[(c + 2) % CH]));
+      }
+      if (OP == 18) asm volatile("lop3.b32 %0, %0, %1, %2, 0xe8;" : "+r"(u[c]) : "r"(u[(c + 1) % CH]), "r"(u[(c + 2) % CH]));
       if (OP == 11) {  // the merge network's shape: min(l, max(l', a)) pairs
         asm volatile("max.f32 %0, %1, %2;" : "=f"(b[c]) : "f"(a[c]), "f"(a[(c + 1) % CH]));
         asm volatile("min.f32 %0, %0, %1;" : "+f"(a[c]) : "f"(b[c]));
@@ -115,6 +137,13 @@ int main() {
   run<9>("FSETP+@IADD", 2, d_out, d_cyc, blocks, threads, iters);
   run<10>("IMNMX", 1, d_out, d_cyc, blocks, threads, iters);
   run<11>("FMNMX max->min pairs", 2, d_out, d_cyc, blocks, threads, iters);
+  run<12>("HMNMX2", 2, d_out, d_cyc, blocks, threads, iters);
+  run<13>("HADD2", 1, d_out, d_cyc, blocks, threads, iters);
+  run<14>("HSETP2+@IADD", 2, d_out, d_cyc, blocks, threads, iters);
+  run<15>("F2FP.F16+FADD", 2, d_out, d_cyc, blocks, threads, iters);
+  run<16>("HMNMX2.BF16", 2, d_out, d_cyc, blocks, threads, iters);
+  run<17>("VIMNMX.S16x2", 2, d_out, d_cyc, blocks, threads, iters);
+  run<18>("LOP3", 1, d_out, d_cyc, blocks, threads, iters);
   cudaError_t e = cudaGetLastError();
   printf("{\"status\": \"%s\"}\n", cudaGetErrorString(e));
   return 0;
