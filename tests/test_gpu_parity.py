@@ -547,3 +547,34 @@ def test_batch_equals_single_calls(n):
                                  for i in range(len(a))])
         assert np.array_equal(batch, single, equal_nan=True), measure
     f.close()
+
+
+def test_bench_launch_configuration_c4_s4096_properties():
+    """The bench's exact launch (C4, n = 1000, all 3 828 region pairs, S = 4096, bench seed) checked
+    on sampled outputs the oracle computes one by one (the full oracle run would take minutes per
+    region): for a few region pairs, the reported argmax is one of the region's sampled point
+    pairs (sampler re-derived by oracle.sample), its oracle value equals the reported max, and no
+    sampled pair drawn at random exceeds it; KSG (k = 3) and Pearson."""
+    spec = synth.spec_of(synth.C4)
+    vals, f = _field(spec)
+    del vals
+    torch.cuda.empty_cache()
+    A, B = synth.context_pairs(synth.bricks_of(synth.C4))
+    S, seed = 4096, 20230907  # bench.py SEED
+    rng = np.random.default_rng(11)
+    sel = rng.choice(len(A), 8, replace=False)
+    for measure, tol in ((cb.CORR_KSG, KSG_TOL), (cb.CORR_PEARSON, PEARSON_TOL)):
+        got_max, got_arg = cb.corr_region_max(f, None, measure, 3, A, B, S, seed)
+        got_max, got_arg = _cpu(got_max), _cpu(got_arg)
+        for r in sel:
+            pairs = [oracle.sample(seed, A[r], B[r], s, spec.nx, spec.ny) for s in range(S)]
+            arg = tuple(int(v) for v in got_arg[r])
+            assert arg in set(pairs), (r, arg)
+            probe = [arg] + [pairs[s] for s in rng.choice(S, 64, replace=False)]
+            pts = sorted({p for ab in probe for p in ab})
+            pos = {p: i for i, p in enumerate(pts)}
+            mini = synth.rows(spec, torch.tensor(pts)).T.contiguous()
+            v = oracle.eval_pairs(mini, None, measure, 3, [pos[a] for a, _ in probe], [pos[b] for _, b in probe])
+            assert abs(v[0] - got_max[r]) <= tol, (r, v[0], got_max[r])
+            assert np.nanmax(v[1:]) <= got_max[r] + tol
+    f.close()
