@@ -73,6 +73,15 @@ def lib():
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(Box), ctypes.POINTER(Box), ctypes.c_int64,
                                         ctypes.c_int64, ctypes.c_uint64, F64P, I64P]
+        L.oracle_region_values.restype = None
+        L.oracle_region_values.argtypes = [F32P, F32P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.POINTER(Box), ctypes.POINTER(Box), ctypes.c_int64,
+                                           ctypes.c_int64, ctypes.c_uint64, F64P, I64P, I64P]
+        L.oracle_sample_many.restype = None
+        L.oracle_sample_many.argtypes = [ctypes.c_uint64, ctypes.POINTER(Box), ctypes.POINTER(Box),
+                                         ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                         ctypes.c_int, I64P, I64P]
         L.oracle_set_threads.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -199,13 +208,14 @@ def _box_points(box, nx, ny):
     return ((z * ny + y) * nx + x).reshape(-1).astype(np.int64)  # local index, x fastest
 
 
-def pearson_block_max(fa, fb, dims, A, B, absval: bool = False, chunk: int = 2048):
+def pearson_block_max(fa, fb, dims, A, B, absval: bool = False, chunk: int = 2048, runner_up: bool = False):
     """Exhaustive Pearson maximum of one region pair -- the PPMCC definition
     (two-pass fp64 means and deviations) for EVERY pair of the two bricks, with
     the |A| x |B| sums of products formed by a library fp64 matmul (a permitted primitive).
     Values rounded to fp32 as the library returns them; NaN (constant series) skipped; ties ->
     lowest q = a_local*|B| + b_local (R16); self pairs skipped with one field.
-    Returns (max, (a, b)) with (nan, (-1, -1)) if no pair is defined."""
+    Returns (max, (a, b)) with (nan, (-1, -1)) if no pair is defined; with runner_up=True also the
+    best value of every OTHER pair (-inf if none), for the argmax-margin check."""
     nx, ny, nz = dims
     fa = _field(fa)
     fbn = fa if fb is None else _field(fb)
@@ -221,6 +231,7 @@ def pearson_block_max(fa, fb, dims, A, B, absval: bool = False, chunk: int = 204
 
     zb, cb = standardise(fbn[:, pb])
     best, arg = np.nan, (-1, -1)
+    tops = []  # the two largest entries of every chunk
     for s in range(0, pa.size, chunk):
         za, ca = standardise(fa[:, pa[s:s + chunk]])
         c = za.T @ zb  # [chunk, |B|] sums of products of deviations / norms
@@ -233,10 +244,16 @@ def pearson_block_max(fa, fb, dims, A, B, absval: bool = False, chunk: int = 204
             c[pa[s:s + chunk][:, None] == pb[None, :]] = np.nan
         c = c.astype(np.float32).astype(np.float64)
         c = np.where(np.isnan(c), -np.inf, c)
+        flat = c.reshape(-1)
+        tops.extend(np.partition(flat, flat.size - 2)[-2:].tolist() if flat.size >= 2 else flat.tolist())
         q = int(np.argmax(c))  # first maximum in row-major (a_local, b_local) order = lowest q
         v = c.reshape(-1)[q]
         if np.isfinite(v) and (np.isnan(best) or v > best):
             best, arg = v, (int(pa[s + q // pb.size]), int(pb[q % pb.size]))
+    if runner_up:
+        tops = sorted(tops)
+        second = tops[-2] if len(tops) >= 2 else -np.inf
+        return best, arg, float(second)
     return best, arg
 
 
@@ -256,3 +273,65 @@ def region_max(fa, fb, dims, measure: int, k: int, regA, regB, samples: int, see
                             measure, int(k), A, B, R, int(samples), ctypes.c_uint64(seed),
                             _p(out, F64P), _p(arg, I64P))
     return out, arg
+
+
+def sample_many(seed: int, regA, regB, count: int, nx: int, ny: int, s0: int = 0):
+    """Sampled point pairs s0 .. s0+count-1 of every region pair (R15): (a, b) int64 [R, count]."""
+    R = len(regA)
+    A = (Box * R)(*[_box(b) for b in regA])
+    B = (Box * R)(*[_box(b) for b in regB])
+    a = np.empty((R, count), np.int64)
+    b = np.empty((R, count), np.int64)
+    lib().oracle_sample_many(ctypes.c_uint64(seed), A, B, R, int(s0), int(count), nx, ny,
+                             _p(a, I64P), _p(b, I64P))
+    return a, b
+
+
+def region_values(fa, fb, dims, measure: int, k: int, regA, regB, samples: int, seed: int):
+    """Every value behind region_max (same enumeration, skips and fp32 rounding): returns
+    (values float64 [R, T], a int64 [R, T], b int64 [R, T]) with T = samples, or |A||B| for the
+    exhaustive case (then all region pairs must have the same box sizes); NaN = skipped."""
+    nx, ny, nz = dims
+    fa = _field(fa)
+    fbn = None if fb is None else _field(fb)
+    n, P = fa.shape
+    assert P == nx * ny * nz
+    R = len(regA)
+    if samples > 0:
+        T = samples
+    else:
+        sz = lambda b: (b[3] - b[0]) * (b[4] - b[1]) * (b[5] - b[2])  # noqa: E731
+        T = sz(regA[0]) * sz(regB[0])
+        assert all(sz(x) * sz(y) == T for x, y in zip(regA, regB))
+    A = (Box * R)(*[_box(b) for b in regA])
+    B = (Box * R)(*[_box(b) for b in regB])
+    out = np.empty((R, T), np.float64)
+    a = np.empty((R, T), np.int64)
+    b = np.empty((R, T), np.int64)
+    lib().oracle_region_values(_p(fa, F32P), None if fbn is None else _p(fbn, F32P), nx, ny, nz, n,
+                               measure, int(k), A, B, R, int(samples), ctypes.c_uint64(seed),
+                               _p(out, F64P), _p(a, I64P), _p(b, I64P))
+    return out, a, b
+
+
+def select_max(values, a, b):
+    """Region maximum from enumerated values (R16): per row, the max over non-NaN
+    values, the argmax at the LOWEST index among equal maxima, and the runner-up = the best value
+    of any entry whose point pair differs from the argmax pair (-inf if none), so that the
+    winning margin is max - runner_up.  All-NaN rows: (nan, (-1, -1), -inf)."""
+    values = np.asarray(values, np.float64)
+    R = values.shape[0]
+    mx = np.full(R, np.nan)
+    arg = np.full((R, 2), -1, np.int64)
+    second = np.full(R, -np.inf)
+    for r in range(R):
+        v = np.where(np.isnan(values[r]), -np.inf, values[r])
+        if not np.isfinite(v).any():
+            continue
+        q = int(np.argmax(v))
+        mx[r] = v[q]
+        arg[r] = (a[r][q], b[r][q])
+        other = (a[r] != a[r][q]) | (b[r] != b[r][q])
+        if other.any():
+            second[r] = np.max(v[other])
+    return mx, arg, second

@@ -312,6 +312,59 @@ void oracle_region_max(const float* fa, const float* fb, int nx, int ny, int nz,
   }
 }
 
+/* Every value behind oracle_region_max, for the argmax-margin checks (the parity bar: the
+ * region argmax must be bit-exact whenever the winning margin exceeds the tolerance, so the
+ * tests need the runner-up).  Same enumeration, skips and fp32 rounding as oracle_region_max
+ * (R11, R16); out[r * total + s] = value of sample s (or exhaustive index q) of
+ * region pair r, NaN where oracle_region_max skips it (self pair, NaN value).  Pair indices
+ * go to out_a / out_b (same layout) when not NULL.  Enumeration only -- no new arithmetic. */
+void oracle_region_values(const float* fa, const float* fb, int nx, int ny, int nz, int n,
+                          int measure, int k, const oracle_box* regA, const oracle_box* regB,
+                          int64_t nregion, int64_t samples, uint64_t seed, double* out,
+                          int64_t* out_a, int64_t* out_b) {
+  int64_t P = (int64_t)nx * ny * nz;
+  int use_abs = (measure & (1 << 9)) != 0;
+  int64_t total = samples > 0 ? samples : box_size(&regA[0]) * box_size(&regB[0]);
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t r = 0; r < nregion; ++r) {
+    for (int64_t s = 0; s < total; ++s) {
+      const oracle_box* A = &regA[r];
+      const oracle_box* B = &regB[r];
+      int64_t nb = box_size(B);
+      int64_t a, b;
+      if (samples > 0) {
+        oracle_sample(seed, A, B, s, nx, ny, &a, &b);
+      } else {
+        a = box_point(A, s / nb, nx, ny);
+        b = box_point(B, s % nb, nx, ny);
+      }
+      double v = ORACLE_NAN;
+      if (!(fb == NULL && a == b)) {
+        v = oracle_pair(fa, fb, P, n, measure, k, a, b);
+        if (!isnan(v)) {
+          if (use_abs) v = fabs(v);
+          v = (double)(float)v;
+        }
+      }
+      out[r * total + s] = v;
+      if (out_a) out_a[r * total + s] = a;
+      if (out_b) out_b[r * total + s] = b;
+    }
+  }
+}
+
+/* The sampled point pairs s = s0 .. s0+count-1 of each region pair (oracle_sample in a loop),
+ * out_a / out_b [nregion][count].  Enumeration only. */
+void oracle_sample_many(uint64_t seed, const oracle_box* regA, const oracle_box* regB,
+                        int64_t nregion, int64_t s0, int64_t count, int nx, int ny,
+                        int64_t* out_a, int64_t* out_b) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < nregion; ++r)
+    for (int64_t s = 0; s < count; ++s)
+      oracle_sample(seed, &regA[r], &regB[r], s0 + s, nx, ny, &out_a[r * count + s],
+                    &out_b[r * count + s]);
+}
+
 /* Host threads used by the OpenMP loops above (not arithmetic: every pair is computed by one
  * thread, so results do not depend on it).  n <= 0 leaves the setting alone.  Returns the
  * thread count the next parallel region will use.  bench.py sets it explicitly because

@@ -89,6 +89,12 @@ def _stream(stream) -> int:
     return int(stream)
 
 
+def _field_stream(field: "Field", stream) -> int:
+    """The caller's stream resolved on the FIELD's device (the library launches on that device)."""
+    with torch.cuda.device(field.device):
+        return _stream(stream)
+
+
 def _ptr(t) -> int:
     if isinstance(t, torch.Tensor):
         return t.data_ptr()
@@ -180,7 +186,7 @@ def corr_eval_pairs(fa: Field, fb: Optional[Field], measure: int, k: int, idxA: 
         out = torch.empty(npairs, dtype=torch.float32, device=idxA.device)
     _check(load().corr_eval_pairs(ctypes.c_void_p(fa.handle), _fb(fb), measure, k, ctypes.c_void_p(_ptr(idxA)),
                                   ctypes.c_void_p(_ptr(idxB)), npairs, ctypes.c_void_p(_ptr(out)),
-                                  ctypes.c_void_p(_stream(stream))))
+                                  ctypes.c_void_p(_field_stream(fa, stream))))
     return out
 
 
@@ -205,7 +211,7 @@ def corr_region_max(fa: Field, fb: Optional[Field], measure: int, k: int, region
         out_argmax = torch.empty((R, 2), dtype=torch.int64, device=dev)
     _check(load().corr_region_max(ctypes.c_void_p(fa.handle), _fb(fb), measure, k, A, B, R, samples,
                                   ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), ctypes.c_void_p(_ptr(out_max)),
-                                  ctypes.c_void_p(_ptr(out_argmax)), ctypes.c_void_p(_stream(stream))))
+                                  ctypes.c_void_p(_ptr(out_argmax)), ctypes.c_void_p(_field_stream(fa, stream))))
     return out_max, out_argmax
 
 
@@ -218,7 +224,7 @@ def corr_ksg_debug(fa: Field, fb: Optional[Field], k: int, idxA: torch.Tensor, i
     _check(load().corr_ksg_debug(ctypes.c_void_p(fa.handle), _fb(fb), k, ctypes.c_void_p(_ptr(idxA)),
                                  ctypes.c_void_p(_ptr(idxB)), npairs, ctypes.c_void_p(_ptr(eps)),
                                  ctypes.c_void_p(_ptr(nx)), ctypes.c_void_p(_ptr(ny)),
-                                 ctypes.c_void_p(_stream(stream))))
+                                 ctypes.c_void_p(_field_stream(fa, stream))))
     return eps, nx, ny
 
 
@@ -243,4 +249,4 @@ launch_count = corr_launch_count
 
 
 def corr_check(field: Field, stream=None):
-    _check(load().corr_check(ctypes.c_void_p(field.handle), ctypes.c_void_p(_stream(stream))))
+    _check(load().corr_check(ctypes.c_void_p(field.handle), ctypes.c_void_p(_field_stream(field, stream))))

@@ -144,3 +144,46 @@ def test_pearson_block_max_matmul_equals_brute_force(absval):
     for r in range(len(A2)):
         v, ab = oracle.pearson_block_max(f, g, (8, 8, 4), A2[r], B2[r])
         assert abs(v - mx[r]) <= 1e-7
+
+
+@pytest.mark.parametrize("measure,samples", [(oracle.KSG, 0), (oracle.KSG, 40), (oracle.PEARSON, 0),
+                                             (oracle.PEARSON | oracle.F_ABS, 25),
+                                             (oracle.KSG | oracle.F_KSG_PLUS1, 0)])
+def test_region_values_select_max_equals_region_max(measure, samples):
+    """The enumeration behind the argmax-margin checks (region_values + select_max) gives the C
+    region_max's maximum and argmax exactly; the runner-up is the best value of any OTHER point
+    pair, checked by brute force over the enumerated list (ties: margin 0)."""
+    spec, f = _c1_field()
+    A, B = synth.context_pairs(synth.bricks_of(synth.C1))
+    mx, arg = oracle.region_max(f, None, (8, 8, 4), measure, 3, A, B, samples, 5)
+    vals, va, vb = oracle.region_values(f, None, (8, 8, 4), measure, 3, A, B, samples, 5)
+    smx, sarg, second = oracle.select_max(vals, va, vb)
+    assert np.array_equal(smx, mx, equal_nan=True) and np.array_equal(sarg, arg)
+    for r in range(len(A)):
+        v = np.where(np.isnan(vals[r]), -np.inf, vals[r])
+        others = [v[t] for t in range(v.size) if (va[r][t], vb[r][t]) != tuple(arg[r])]
+        assert second[r] == (max(others) if others else -np.inf)
+        assert second[r] <= smx[r]
+        if samples:
+            ab = [oracle.sample(5, A[r], B[r], s, 8, 8) for s in range(samples)]
+            assert ab == list(zip(va[r].tolist(), vb[r].tolist()))
+
+
+def test_sample_many_equals_sample():
+    A, B = synth.context_pairs(synth.bricks_of(synth.C3))
+    A, B = A[::97], B[::97]
+    a, b = oracle.sample_many(11, A, B, 30, 250, 352, s0=7)
+    for r in range(len(A)):
+        for s in range(30):
+            assert oracle.sample(11, A[r], B[r], 7 + s, 250, 352) == (a[r, s], b[r, s])
+
+
+def test_pearson_block_runner_up_brute_force():
+    spec, f = _c1_field()
+    boxes = synth.bricks_of(synth.C1)
+    A, B = synth.context_pairs(boxes)
+    vals, va, vb = oracle.region_values(f, None, (8, 8, 4), oracle.PEARSON, 0, A, B, 0, 0)
+    _, _, second = oracle.select_max(vals, va, vb)
+    for r in range(len(A)):
+        v, ab, sec = oracle.pearson_block_max(f, None, (8, 8, 4), A[r], B[r], chunk=5, runner_up=True)
+        assert abs(sec - second[r]) <= 1e-7 and sec <= v
