@@ -118,9 +118,8 @@ int alloc_field(int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t dev
   return CORR_OK;
 }
 
-int ksg_flags(int32_t measure) {
-  return ((measure & CORR_F_KSG_PLUS1) ? 1 : 0) | ((measure & CORR_F_KSG_DENSE) ? 2 : 0);
-}
+bool ksg_plus1(int32_t measure) { return (measure & CORR_F_KSG_PLUS1) != 0; }
+KsgPath ksg_path(int32_t measure) { return (measure & CORR_F_KSG_DENSE) ? kKsgDense : kKsgAuto; }
 
 // Copies member-major values (host or device) into f and rebuilds every derived buffer on `st`;
 // synchronises `st` (input validation).  The non-finite flag lives in err[1], the index-range
@@ -385,7 +384,7 @@ static int eval_pairs_impl(const corr_field* fa, const corr_field* fb, int32_t m
   cudaStream_t st = (cudaStream_t)cuda_stream;
   cudaError_t e;
   if ((measure & 0xFF) == CORR_KSG) {
-    e = launch_ksg(fa, fb, k, ksg_flags(measure), src, po, st);
+    e = launch_ksg(fa, fb, k, ksg_plus1(measure), ksg_path(measure), src, po, st);
     if (e == cudaErrorNotSupported) return fail(CORR_E_INVAL, "KSG with k > 32 is not supported");
   } else {
     e = launch_pearson_pairs(fa, fb, src, po, st);
@@ -482,7 +481,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
   po.absval = (measure & CORR_F_ABS) != 0;
   if (e == cudaSuccess) {
     if ((measure & 0xFF) == CORR_KSG) {
-      e = launch_ksg(fa, fb, k, ksg_flags(measure), src, po, st);
+      e = launch_ksg(fa, fb, k, ksg_plus1(measure), ksg_path(measure), src, po, st);
       if (e == cudaErrorNotSupported) {
         if (own_reg) cudaFreeAsync(dreg, st);
         cudaFreeAsync(keys, st);

@@ -72,9 +72,16 @@ struct PairOut {
 // ---- launchers (defined in the .cu files) ----
 cudaError_t launch_field_ingest(corr_field* f, const float* dvalues_member_major, cudaStream_t st);
 cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int fx, int fy, int fz, cudaStream_t st);
-// plus1: bit 0 = psi(n+1) variant, bit 1 = dense (no sweep)
-cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1,
+// Which k-NN formulation launch_ksg runs (all give bit-identical eps / counts / MI):
+//   kKsgAuto  -- column-cell kernel for 128 <= n, k <= 8 (ksg_cell.cu), else the sweep / warp /
+//                batched kernels of ksg.cu;
+//   kKsgDense -- every n(n-1) comparison (CORR_F_KSG_DENSE);
+//   kKsgSweep -- the round-1 x-sorted exact sweep (A/B reference; env CORR_KSG_PATH=sweep).
+enum KsgPath { kKsgAuto = 0, kKsgDense = 1, kKsgSweep = 2 };
+cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool plus1, KsgPath path,
                        const PairSrc& src, const PairOut& out, cudaStream_t st);
+cudaError_t launch_ksg_cell(const corr_field* fa, const corr_field* fb, int k, bool plus1, const PairSrc& src,
+                            const PairOut& out, cudaStream_t st);
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset);
 // Device copy of a small host table (region lists) that stays resident and is reused when the
 // same bytes come again: no host->device copy on the call path of repeated calls.  (A small copy

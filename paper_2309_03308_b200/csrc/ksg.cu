@@ -30,38 +30,13 @@
 
 #include <algorithm>
 
-#include "sampler.cuh"
+#include "ksg_common.cuh"
 
 namespace corr {
 
 __device__ unsigned long long g_ksg_comparisons;  // executed comparisons (corr_ksg_comparisons)
 
 namespace {
-
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-  unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a);
-  unsigned long long ub = *reinterpret_cast<unsigned long long*>(&b);
-  unsigned long long ud;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ud) : "l"(ua), "l"(ub));
-  return *reinterpret_cast<float2*>(&ud);
-}
-
-__device__ __forceinline__ float cheb(float2 zi, float2 zj) {
-  const float2 d = sub2(zi, zj);
-  return fmaxf(fabsf(d.x), fabsf(d.y));
-}
-
-template <int K>
-__device__ __forceinline__ void merge2(float (&l)[K], float d0, float d1) {
-  const float a = fminf(d0, d1), b = fmaxf(d0, d1);
-  float nl[K];
-  nl[0] = fminf(l[0], a);
-  if (K >= 2) nl[1] = fminf(fminf(l[1], fmaxf(l[0], a)), b);
-#pragma unroll
-  for (int r = 2; r < K; ++r) nl[r] = fminf(fminf(l[r], fmaxf(l[r - 1], a)), fmaxf(l[r - 2], b));
-#pragma unroll
-  for (int r = 0; r < K; ++r) l[r] = nl[r];
-}
 
 // Strict marginal count of a member with value v and radius e on a sorted
 // array S (element stride ST): #{j != i : |fl(v - S_j)| < e}.
@@ -70,13 +45,6 @@ __device__ __forceinline__ void merge2(float (&l)[K], float d0, float d1) {
 //           are monotone in s by monotone rounding, and imply / cover s >= v because e > 0);
 //           [w, u) holds every s with |fl(s - v)| < e, the member itself included -> u - w - 1.
 // Branch-free lower bounds (uniform trip count), the two searches interleaved for ILP.
-template <int OFF>
-__device__ __forceinline__ float lds_imm(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
-  return v;
-}
-
 // The four searches of one member (u and w on the sorted marginal x -- stride 8 B inside xy --
 // and on the sorted y row), interleaved; step 2^B is a compile-time immediate offset.
 template <int B>
@@ -132,13 +100,6 @@ __device__ __forceinline__ void own_chunk(const float4* __restrict__ cp, const f
       merge2<K>(l[rr], e0, e1);
     }
   }
-}
-
-template <int K>
-__device__ __forceinline__ void insert1(float (&l)[K], float d) {
-#pragma unroll
-  for (int t = K - 1; t >= 1; --t) l[t] = fminf(l[t], fmaxf(l[t - 1], d));
-  l[0] = fminf(l[0], d);
 }
 
 // RM == 1 own chunk without masks: lane L reads the warp's 32 joint samples rotated by L
@@ -315,49 +276,6 @@ __device__ __forceinline__ void chunk_adjacent(const float4* __restrict__ cp, co
       merge2<K>(l[0], d[2], d[3]);
     }
   }
-}
-
-// ---- a2 staging through the TMA unit: 1-D bulk copies global -> shared with an mbarrier
-// (cp.async.bulk, contiguous rows: no tensor map needed) and bulk L2 prefetches of the
-// next pair's rows, so a CTA's next staging finds its rows in L2.
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void bar_init(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(b)));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(b))
-               : "memory");
-}
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
-// Side-effect-free peek at unit u's point pair (prefetch only; errors are raised when the
-// unit itself is processed).
-__device__ __forceinline__ bool peek_pair(const PairSrc& s, int64_t u, int64_t& a, int64_t& b) {
-  if (s.mode == kList) {
-    a = s.idxA[u];
-    b = s.idxB[u];
-    return a >= 0 && a < s.P && b >= 0 && b < s.P;
-  }
-  int64_t r;
-  uint32_t idx;
-  return unit_pair(s, u, a, b, r, idx);
 }
 
 // ---- a3 / a4 / a5 for one member block (32*RM sort-consecutive members) of a staged pair:
@@ -948,9 +866,17 @@ cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus
 
 }  // namespace
 
-cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int plus1, const PairSrc& src,
-                       const PairOut& out, cudaStream_t st) {
+cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool plus1_flag, KsgPath path,
+                       const PairSrc& src, const PairOut& out, cudaStream_t st) {
   if (src.nunits == 0) return cudaSuccess;
+  static const bool env_sweep = [] {
+    const char* v = getenv("CORR_KSG_PATH");
+    return v && v[0] == 's';
+  }();
+  if (path == kKsgAuto && env_sweep) path = kKsgSweep;
+  if (path == kKsgAuto && fa->n > kWarpKernelMaxN && k <= 8) return launch_ksg_cell(fa, fb, k, plus1_flag, src, out, st);
+  // internal plumbing of the ksg.cu launchers: bit 0 = psi(n+1) variant, bit 1 = dense
+  const int plus1 = (plus1_flag ? 1 : 0) | (path == kKsgDense ? 2 : 0);
   switch (k) {
     case 1: return launch_k<1>(fa, fb, k, plus1, src, out, st);
     case 2: return launch_k<2>(fa, fb, k, plus1, src, out, st);
@@ -983,12 +909,17 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, int pl
   return cudaErrorNotSupported;
 }
 
+cudaError_t ksg_cell_comparisons(unsigned long long* value, bool reset);
+
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset) {
   cudaError_t e = cudaMemcpyFromSymbol(value, g_ksg_comparisons, sizeof(unsigned long long));
   if (e == cudaSuccess && reset) {
     const unsigned long long zero = 0;
     e = cudaMemcpyToSymbol(g_ksg_comparisons, &zero, sizeof(zero));
   }
+  unsigned long long cell = 0;
+  if (e == cudaSuccess) e = ksg_cell_comparisons(&cell, reset);
+  *value += cell;
   return e;
 }
 

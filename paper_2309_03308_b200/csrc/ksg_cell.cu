@@ -1,0 +1,392 @@
+// ksg_cell.cu -- Kraskov (KSG) MI of point pairs with a column-cell k-NN (round 2 default for
+// 128 <= n and k <= 8).  SURVEY.md §8(a) rows a2-a5; PAPER.md:172-174 (Eq. 2), readings R1-R7.
+//
+// The paper builds a k-d tree per pair; the round-1 kernel scanned the
+// pair's x-sorted order outward from 32-member blocks (exact sweep), executing ~169 candidate
+// distances per member because the 32 lanes of a warp advance over the same candidates.  Here
+// each member scans ITS OWN candidates, in a two-level structure built per pair in shared memory:
+//
+//   x = the wider marginal (KSG is symmetric in x and y, Eq. 1).  Columns = 32 consecutive
+//   x-ranks; inside a column the members are kept in y order (a stable multisplit of the y-sorted
+//   row by column).  cellstart[c][g] = number of column-c members whose y-rank is < 32 g.
+//
+//   A warp owns a column (lane = member in the column's y order):
+//     own column  -- scan up (p+1, p+2, ...) and down (p-1, ...) in y order, one candidate per
+//                    direction per step, merged into the register k-list; a direction stops once
+//                    fl(y_j - y_i) >= l[k-1] (every further candidate is at least as far in y, so
+//                    none can enter the list: monotone rounding, the list only shrinks);
+//     neighbour columns, nearest first, alternating sides -- a lane needs column c' iff the x-gap
+//                    to its nearest edge is < l[k-1] (the round-1 sweep test); the side ends when
+//                    no lane needs it.  Needing lanes start at cellstart[c'][y-band of the member]
+//                    (no search: the member's position in c' lies inside that cell) and scan
+//                    up / down with the same stop rule.
+//   Candidates of other columns are real members, so any extra candidate is harmless (the
+//   k-smallest multiset over a superset that contains every candidate below the final eps is
+//   exact); the self pair is never visited.  Column ends hold sentinels (+inf, -inf) / (+inf,
+//   +inf) so a scan stops there without bounds checks, and a stopped direction stays on its stop
+//   candidate (re-merging a value >= l[k-1] is a no-op).
+//
+// Counts (a4) are the round-1 binary searches on the two sorted rows; psi / reduction as before.
+#include "ksg_common.cuh"
+
+namespace corr {
+
+// executed comparisons of this kernel (no relocatable device code: ksg.cu's counter is not
+// visible here; ksg_comparisons() reads both)
+__device__ unsigned long long g_ksg_cell_comparisons;
+
+namespace {
+
+constexpr int kCS = 34;  // float2 entries per column: lo sentinel, 32 members, hi sentinel
+
+struct CellLayout {
+  int n, n_pad, nch, nseg, nsx, log2p;
+  uint32_t o_su, o_sv, o_col, o_pu, o_pv, o_xr, o_cs, o_cols, o_red, o_misc, bytes;
+};
+
+__host__ __device__ inline CellLayout cell_layout(int n, int n_pad, int nw) {
+  CellLayout L;
+  L.n = n;
+  L.n_pad = n_pad;
+  L.nch = (n + 31) >> 5;
+  L.nseg = L.nch;
+  int log2p = 1;
+  while ((1 << log2p) <= n) ++log2p;  // 2^log2p > n: +inf padded search arrays
+  L.log2p = log2p;
+  L.nsx = n_pad > (1 << log2p) ? n_pad : (1 << log2p);
+  uint32_t o = 0;
+  auto take = [&](uint32_t bytes, uint32_t align) {
+    o = (o + align - 1) / align * align;
+    const uint32_t r = o;
+    o += bytes;
+    return r;
+  };
+  L.o_su = take(L.nsx * 4u, 16);
+  L.o_sv = take(L.nsx * 4u, 16);
+  L.o_col = take(((uint32_t)L.nch * kCS + 2u) * 8u, 16);  // + one pad entry before and after
+  L.o_pu = take(n_pad * 2u, 16);
+  L.o_pv = take(n_pad * 2u, 16);
+  L.o_xr = take(n_pad * 2u, 16);
+  L.o_cs = take((uint32_t)L.nch * (L.nseg + 1) * 2u, 16);
+  L.o_cols = take((uint32_t)L.nch * 32u * 2u, 16);
+  L.o_red = take((uint32_t)nw * 8u, 8);
+  L.o_misc = take(16, 8);  // next_blk (int) + staging mbarrier (u64)
+  L.bytes = (o + 15) / 16 * 16;
+  return L;
+}
+
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ float chebd(float2 d) { return fmaxf(fabsf(d.x), fabsf(d.y)); }
+
+// Lockstep up / down scan of one column for the whole warp, one candidate per direction per
+// step.  A direction stops once fl(y_j - y_i) >= l[K-1]; its pointer then rests on that
+// candidate, whose distance is >= l[K-1] (re-merging it is a no-op).  Column ends hold
+// sentinels (infinite distance, immediate stop).  Lanes that do not need the column start on the
+// sentinels.
+template <int K>
+__device__ __forceinline__ void scan_column(uint32_t& pu, uint32_t& pd, float2 zi, float (&l)[K]) {
+#pragma unroll 1
+  while (true) {
+    const float2 zu = lds_f2(pu), zd = lds_f2(pd);
+    const float2 du = sub2(zi, zu), dd = sub2(zi, zd);
+    merge2<K>(l, chebd(du), chebd(dd));
+    const bool su = -du.y >= l[K - 1];  // fl(y_j - y_i) = -fl(y_i - y_j) exactly
+    const bool sd = dd.y >= l[K - 1];
+    pu += su ? 0u : 8u;
+    pd -= sd ? 0u : 8u;
+    if (__all_sync(0xffffffffu, su && sd)) break;
+  }
+}
+
+// Strict marginal counts on the two sorted rows (stride 4 B, +inf padded to
+// 2^log2p): the round-1 monotone-predicate binary searches (ksg.cu), both arrays float.
+template <int B>
+struct CountSearch44 {
+  __device__ __forceinline__ static void run(int log2p, uint32_t& xu, uint32_t& xw, uint32_t& yu, uint32_t& yw,
+                                             float x, float y, float e) {
+    if (B < log2p) {
+      constexpr int ST = (1 << B) * 4;
+      const float pxu = lds_imm<ST - 4>(xu), pxw = lds_imm<ST - 4>(xw);
+      const float pyu = lds_imm<ST - 4>(yu), pyw = lds_imm<ST - 4>(yw);
+      xu = (pxu - x >= e) ? xu : xu + ST;
+      xw = (x - pxw < e) ? xw : xw + ST;
+      yu = (pyu - y >= e) ? yu : yu + ST;
+      yw = (y - pyw < e) ? yw : yw + ST;
+    }
+    CountSearch44<B - 1>::run(log2p, xu, xw, yu, yw, x, y, e);
+  }
+};
+template <>
+struct CountSearch44<-1> {
+  __device__ __forceinline__ static void run(int, uint32_t&, uint32_t&, uint32_t&, uint32_t&, float, float, float) {}
+};
+
+template <int K, int NW>
+__global__ void __launch_bounds__(NW * 32, (NW == 4 ? 8 : 4)) ksg_cell_kernel(
+    const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Sb,
+    const uint16_t* __restrict__ Pb, const float* __restrict__ spa, const float* __restrict__ spb,
+    const uint8_t* __restrict__ ca, const uint8_t* __restrict__ cb, const double* __restrict__ psi, int n, int n_pad,
+    int k, int plus1, PairSrc src, PairOut out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const CellLayout L = cell_layout(n, n_pad, NW);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  constexpr int NT = NW * 32;
+  const int nch = L.nch, nseg = L.nseg, cs_stride = L.nseg + 1;
+  float* su = reinterpret_cast<float*>(smem + L.o_su);
+  float* sv = reinterpret_cast<float*>(smem + L.o_sv);
+  float2* col = reinterpret_cast<float2*>(smem + L.o_col) + 1;  // col[-1] and col[nch*kCS] are pads
+  uint16_t* pu_s = reinterpret_cast<uint16_t*>(smem + L.o_pu);
+  uint16_t* pv_s = reinterpret_cast<uint16_t*>(smem + L.o_pv);
+  uint16_t* xr = reinterpret_cast<uint16_t*>(smem + L.o_xr);
+  uint16_t* rk = pu_s;  // rank inside the cell, per y-rank s (pu_s is dead once xr is built)
+  uint16_t* cs = reinterpret_cast<uint16_t*>(smem + L.o_cs);
+  uint16_t* cols = reinterpret_cast<uint16_t*>(smem + L.o_cols);  // y-rank s of each column entry
+  double* red = reinterpret_cast<double*>(smem + L.o_red);
+  int* next_blk = reinterpret_cast<int*>(smem + L.o_misc);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.o_misc + 8);
+  const uint32_t col_base = su32(col), su_base = su32(su), sv_base = su32(sv), cs_base = su32(cs),
+                 cols_base = su32(cols);
+
+  for (int t = n_pad + tid; t < L.nsx; t += NT) su[t] = sv[t] = INFINITY;  // never overwritten
+  if (tid == 0) col[-1] = col[nch * kCS] = make_float2(INFINITY, INFINITY);
+  if (tid == 0) bar_init(bar);
+  __syncthreads();
+  uint32_t phase = 0;
+  const uint32_t row_bytes = (uint32_t)n_pad * 4u;
+  const double psi_nk = __ldg(psi + n) + __ldg(psi + k);
+  const int off = plus1 ? 1 : 0;
+  unsigned long long executed = 0;
+
+  for (int64_t u = blockIdx.x; u < src.nunits; u += gridDim.x) {
+    int64_t a, b, r;
+    uint32_t idx;
+    const bool ok = unit_pair(src, u, a, b, r, idx);
+    if (!ok) {
+      if (src.mode == kList && tid == 0) out.out[u] = NAN;
+      continue;
+    }
+    const bool degenerate = (ca[a] | cb[b]) != 0;
+    if (degenerate && out.dbg_eps == nullptr) {
+      if (src.mode == kList && tid == 0) out.out[u] = NAN;
+      continue;
+    }
+    const bool swap = spb[b] > spa[a];  // x = the wider marginal
+    const float* Su = swap ? Sb + b * n_pad : Sa + a * n_pad;
+    const uint16_t* Pu = swap ? Pb + b * n_pad : Pa + a * n_pad;
+    const float* Sv = swap ? Sa + a * n_pad : Sb + b * n_pad;
+    const uint16_t* Pv = swap ? Pa + a * n_pad : Pb + b * n_pad;
+    __syncthreads();  // the previous pair is done with every shared array
+    if (tid == 0) {
+      *next_blk = NW;  // columns 0 .. NW-1 are taken statically
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_expect(bar, 2u * row_bytes + row_bytes);
+      bulk_g2s(su, Su, row_bytes, bar);
+      bulk_g2s(sv, Sv, row_bytes, bar);
+      bulk_g2s(pu_s, Pu, row_bytes / 2u, bar);
+      bulk_g2s(pv_s, Pv, row_bytes / 2u, bar);
+      int64_t a2, b2;  // the next pair stages S and perm of both of its points, whichever is x
+      if (u + gridDim.x < src.nunits && peek_pair(src, u + gridDim.x, a2, b2)) {
+        bulk_prefetch_l2(Sa + a2 * n_pad, row_bytes);
+        bulk_prefetch_l2(Sb + b2 * n_pad, row_bytes);
+        bulk_prefetch_l2(Pa + a2 * n_pad, row_bytes / 2u);
+        bulk_prefetch_l2(Pb + b2 * n_pad, row_bytes / 2u);
+      }
+    }
+    for (int q = tid; q < nch * cs_stride; q += NT) cs[q] = 0;
+    bar_wait(bar, phase);
+    phase ^= 1u;
+    // ---- build: x-rank of every member, stable multisplit of the y order by column ----
+    for (int t = tid; t < n; t += NT) xr[pu_s[t]] = (uint16_t)t;
+    __syncthreads();
+    for (int g = warp; g < nseg; g += NW) {
+      const int s = 32 * g + lane;
+      const bool valid = s < n;
+      const int c = valid ? (xr[pv_s[s]] >> 5) : 0xFFFF;
+      const unsigned peers = __match_any_sync(0xffffffffu, c);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      if (valid) {
+        rk[s] = (uint16_t)rank;
+        if (rank == 0) cs[c * cs_stride + g] = (uint16_t)__popc(peers);
+      }
+    }
+    __syncthreads();
+    for (int c = warp; c < nch; c += NW) {  // exclusive prefix over the y-segments of column c
+      int carry = 0;
+      for (int g0 = 0; g0 < nseg; g0 += 32) {
+        const int g = g0 + lane;
+        const int v = g < nseg ? cs[c * cs_stride + g] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        if (g < nseg) cs[c * cs_stride + g] = (uint16_t)(carry + incl - v);
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    __syncthreads();
+    for (int s = tid; s < n; s += NT) {
+      const int t = xr[pv_s[s]];
+      const int c = t >> 5;
+      const int pos = cs[c * cs_stride + (s >> 5)] + rk[s];
+      col[c * kCS + 1 + pos] = make_float2(su[t], sv[s]);
+      cols[c * 32 + pos] = (uint16_t)s;
+    }
+    for (int c = tid; c < nch; c += NT) {
+      col[c * kCS] = make_float2(INFINITY, -INFINITY);
+      const int v = min(32, n - 32 * c);
+      for (int q = v; q < 33; ++q) col[c * kCS + 1 + q] = make_float2(INFINITY, INFINITY);
+    }
+    __syncthreads();
+
+    // ---- a3: one column per warp (first static, then dynamic), lockstep scans ----
+    double acc = 0.0;
+    {
+      int ncand = 0;
+      for (int c = warp; c < nch;) {
+        const int v = min(32, n - 32 * c);
+        const bool active = lane < v;
+        const uint32_t cb0 = col_base + (uint32_t)(c * kCS) * 8u;
+        // lanes without a member take (0, 0): finite, so their scans stop on the sentinels at once
+        const float2 zi = active ? lds_f2(cb0 + (uint32_t)(1 + lane) * 8u) : make_float2(0.f, 0.f);
+        const int band = active ? (int)lds_u16(cols_base + (uint32_t)(c * 32 + lane) * 2u) >> 5 : 0;
+        float l[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) l[t] = INFINITY;
+        // own column: up from p+1, down from p-1 (lanes without a member start on the sentinels)
+        uint32_t pu = active ? cb0 + (uint32_t)(lane + 2) * 8u : cb0 + 33u * 8u;
+        uint32_t pd = active ? cb0 + (uint32_t)lane * 8u : cb0;
+        scan_column<K>(pu, pd, zi, l);
+        // executed comparisons: the visited entries [pd, pu] minus the member itself and sentinels
+        if (active) ncand += (int)((pu - pd) >> 3) - (pu == cb0 + 33u * 8u) - (pd == cb0);
+        // neighbour columns, nearest first, alternating sides; a side ends at the first column no
+        // lane needs (its x-gap only grows outward, the lists only shrink)
+        int lo = c - 1, hi = c + 1, dir = 0;
+#pragma unroll 1
+        while (lo >= 0 || hi < nch) {
+          const bool right = lo < 0 || (hi < nch && dir);
+          dir ^= 1;
+          const int cc = right ? hi : lo;
+          const float xe = lds_f32(su_base + (uint32_t)(32 * cc + (right ? 0 : 31)) * 4u);
+          const float gap = right ? xe - zi.x : zi.x - xe;
+          const bool need = active && gap < l[K - 1];
+          if (!__any_sync(0xffffffffu, need)) {
+            if (right) hi = nch; else lo = -1;
+            continue;
+          }
+          const uint32_t nb0 = col_base + (uint32_t)(cc * kCS) * 8u;
+          const uint32_t start = lds_u16(cs_base + (uint32_t)(cc * cs_stride + band) * 2u);
+          pu = need ? nb0 + (1u + start) * 8u : nb0 + 33u * 8u;
+          pd = need ? nb0 + start * 8u : nb0;
+          scan_column<K>(pu, pd, zi, l);
+          if (need) ncand += (int)((pu - pd) >> 3) + 1 - (pu == nb0 + 33u * 8u) - (pd == nb0);
+          if (right) ++hi; else --lo;
+        }
+        int nb = 0;
+        if (lane == 0) nb = atomicAdd(next_blk, 1);  // claim the next column (latency hides below)
+        // ---- a4 / a5: strict marginal counts (binary searches on the sorted rows) and psi ----
+        if (active) {
+          const float e = l[K - 1];
+          int cx = 0, cy = 0;
+          if (e > 0.f) {
+            uint32_t xu = su_base, xw = su_base, yu = sv_base, yw = sv_base;
+            CountSearch44<12>::run(L.log2p, xu, xw, yu, yw, zi.x, zi.y, e);
+            cx = (int)((xu - xw) >> 2) - 1;
+            cy = (int)((yu - yw) >> 2) - 1;
+          }
+          acc += __ldg(psi + cx + off) + __ldg(psi + cy + off);
+          if (out.dbg_eps) {
+            const int m = pv_s[cols[c * 32 + lane]];
+            out.dbg_eps[u * n + m] = e;
+            out.dbg_nx[u * n + m] = swap ? cy : cx;
+            out.dbg_ny[u * n + m] = swap ? cx : cy;
+          }
+        }
+        c = __shfl_sync(0xffffffffu, nb, 0);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
+      if (lane == 0) executed += (unsigned long long)ncand;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < NW; ++w) s += red[w];
+      const float mi = degenerate ? NAN : (float)(psi_nk - s / (double)n);
+      if (src.mode == kList) {
+        out.out[u] = mi;
+      } else if (!isnan(mi)) {
+        atomicMax(out.keys + r, pack_key(out.absval ? fabsf(mi) : mi, idx));
+      }
+    }
+  }
+  if (lane == 0 && executed) atomicAdd(&g_ksg_cell_comparisons, executed);
+}
+
+template <int K, int NW>
+cudaError_t launch_cell_t(const corr_field* fa, const corr_field* fb, int k, bool plus1, const PairSrc& src,
+                          const PairOut& out, cudaStream_t st) {
+  const CellLayout L = cell_layout(fa->n, fa->n_pad, NW);
+  auto kern = ksg_cell_kernel<K, NW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, L.bytes);
+  if (occ < 1) occ = 1;
+  int64_t blocks = src.nunits;
+  const int64_t cap = (int64_t)kSMs * occ;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, NW * 32, L.bytes, st>>>(fa->S, fa->perm, fb->S, fb->perm, fa->spread, fb->spread, fa->cflag,
+                                                   fb->cflag, fa->psi, fa->n, fa->n_pad, k, plus1 ? 1 : 0, src, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t ksg_cell_comparisons(unsigned long long* value, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(value, g_ksg_cell_comparisons, sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long zero = 0;
+    e = cudaMemcpyToSymbol(g_ksg_cell_comparisons, &zero, sizeof(zero));
+  }
+  return e;
+}
+
+// Column-cell KSG for 128 <= n <= 4096, k <= 8 (register lists of K = k entries).
+cudaError_t launch_ksg_cell(const corr_field* fa, const corr_field* fb, int k, bool plus1, const PairSrc& src,
+                            const PairOut& out, cudaStream_t st) {
+  switch (k) {
+    case 1: return launch_cell_t<1, 4>(fa, fb, k, plus1, src, out, st);
+    case 2: return launch_cell_t<2, 4>(fa, fb, k, plus1, src, out, st);
+    case 3: return launch_cell_t<3, 4>(fa, fb, k, plus1, src, out, st);
+    case 4: return launch_cell_t<4, 4>(fa, fb, k, plus1, src, out, st);
+    case 5: return launch_cell_t<5, 4>(fa, fb, k, plus1, src, out, st);
+    case 6: return launch_cell_t<6, 4>(fa, fb, k, plus1, src, out, st);
+    case 7: return launch_cell_t<7, 4>(fa, fb, k, plus1, src, out, st);
+    case 8: return launch_cell_t<8, 4>(fa, fb, k, plus1, src, out, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace corr
