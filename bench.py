@@ -11,8 +11,9 @@ hot path over the context view:
     +  all-gather of the shards' maxima over NCCL (a10, N > 1).
 `value` = KSG point pairs evaluated per second by the whole job (max-over-ranks device
 time), inputs resident in HBM.  `e2e` = the same metric through the C ABI starting from
-HOST memory: per step the 7 GB member-major field is copied from pinned host memory,
-ingested (corr_field_create), the step runs, and the maxima are read back to the host.
+HOST memory: per step the pinned host pointer of the 7 GB member-major field is passed to
+corr_field_update (the library streams and re-ingests it), the step runs, and the maxima are
+read back to the host.  `ingest` = the field ingest kernels' achieved HBM bandwidth.
 
 `--impl reference` times the CPU oracle (oracle/, plain C + OpenMP) as it stands on the
 box's host cores on a bounded sample of the same workload (the reference arm for this
@@ -253,6 +254,24 @@ def main():
     stream = torch.cuda.current_stream()
     ev = {"ksg": [], "pearson_sampled": [], "pearson_block": []}
 
+    # field ingest (row a1, HBM-bound): corr_field_update from the device-resident input --
+    # transpose [n][P] -> F[P][n_pad], fp64 stats + Z / tf32 split / bf16 planes, per-row sort
+    n_pad_ = (spec.members + 7) // 8 * 8
+    P_ = spec.points
+    ing_bytes = {"transpose": P_ * (4 * spec.members + 4 * n_pad_),
+                 "stats": P_ * (4 * spec.members + (4 + 4 + 4 + 2) * n_pad_),
+                 "sort": P_ * (4 * spec.members + (4 + 2) * n_pad_)}
+    cb.corr_field_update(field, vals)
+    torch.cuda.synchronize()
+    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    i0.record(stream)
+    for _ in range(3):
+        cb.corr_field_update(field, vals)
+    i1.record(stream)
+    torch.cuda.synchronize()
+    cb.corr_check(field)
+    ing_ms = i0.elapsed_time(i1) / 3
+
     def _ev():
         e = torch.cuda.Event(enable_timing=True)
         e.record(stream)
@@ -273,11 +292,8 @@ def main():
         if world > 1:
             km, ka = cdist.gather_region_results(km, ka, bounds)
             pm, pa = cdist.gather_region_results(pm, pa, bounds)
-            fparts = [torch.empty((1, 3), dtype=torch.int64, device=fm.device) for _ in range(world)]
-            packed = torch.cat([fm.view(torch.int32).to(torch.int64).view(1, 1), fa.view(1, 2)], 1)
-            cdist.all_gather(fparts, packed)
-            fm = torch.stack([p[0, 0].to(torch.int32).view(torch.float32) for p in fparts])
-            fa = torch.stack([p[0, 1:] for p in fparts])
+            # the focus pair's slabs: one all-reduce MAX over packed (value, q) keys, on the device
+            fm, fa = cdist.combine_focus_device(fm, fa, slabs, fB, spec.nx, spec.ny)
         return km, ka, pm, pa, fm, fa
 
     for _ in range(args.warmup):
@@ -301,7 +317,6 @@ def main():
     t1.record(stream)
     torch.cuda.synchronize()
     launches = cb.launch_count() - l0
-    executed = cb.corr_ksg_comparisons(local, reset=True) / args.steps
     gemm_bf16, gemm_tf32 = (v / args.steps for v in cb.corr_gemm_flops(local, reset=True))
     if world > 1:
         tdist.barrier()
@@ -316,24 +331,32 @@ def main():
     total_pairs = R * S
     value = total_pairs / (ms / 1e3)
 
-    # roofline of the dominant kernel (KSG, ALU-bound).  The exact sweep skips comparisons that
-    # cannot change any eps_i, so the per-unit figure is the EXECUTED member-comparisons
-    # ("report pairs/s and executed comparisons, never dense-equivalent").
+    # roofline of the dominant kernel (KSG, ALU-bound).  The column-cell k-NN skips every
+    # comparison that provably cannot change an eps_i, so the per-unit figure is the EXECUTED
+    # member-comparisons ("report pairs/s and executed comparisons, never
+    # dense-equivalent"), tallied by one extra, untimed launch of the same shard with
+    # CORR_F_KSG_COUNT (the counting build; the timed kernel does not count).
     n = spec.members
     my_pairs = (hi - lo) * S
     ksg_ms = stage_ms["ksg"]
+    torch.cuda.synchronize()
+    cb.corr_ksg_comparisons(local, reset=True)
+    cb.corr_region_max(field, None, cb.CORR_KSG | cb.CORR_F_KSG_COUNT, K_NN, Ash, Bsh, S, SEED)
+    executed = cb.corr_ksg_comparisons(local, reset=True)
     achieved = executed / (ksg_ms / 1e3)
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
     sm_max = peaks.get("sm_max_mhz") or clk.get("sm_max_mhz") or 1965.0
     peak = 148 * 128 * sm_max * 1e6 / 4.0
     traffic = None
+    ncu_ctx = {}
     if os.path.exists(NCU_TRAFFIC):
         try:
             tr = json.load(open(NCU_TRAFFIC))
             traffic = tr.get("ksg_dram_bytes_per_pair", 0) * my_pairs or None
+            ncu_ctx = {k: tr[k] for k in ("ksg_kernel", "alu_pipe_pct", "issue_active_pct", "source") if k in tr}
         except Exception:
             traffic = None
-    roofline = {"bound": "alu", "kernel": "ksg_sorted_kernel<3,1,sweep> (k-NN + counts + psi)",
+    roofline = {"bound": "alu", "kernel": f"ksg_cell_kernel<{K_NN},4> (column-cell k-NN + counts + psi)",
                 "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcmp/s", "frac": achieved / peak,
                 "traffic": traffic,
                 "peak_basis": f"148 SMs x 128 fp32 lanes x {sm_max:.0f} MHz / 4 ops per member-comparison",
@@ -341,7 +364,10 @@ def main():
                                            if clk.get("sm_mhz") else None),
                 "executed_comparisons_per_pair": executed / max(my_pairs, 1),
                 "dense_comparisons_per_pair": n * (n - 1),
-                "ksg_ms_per_step": ksg_ms, "algorithmic_bytes_per_pair": 14 * spec.members}
+                "ksg_ms_per_step": ksg_ms, "algorithmic_bytes_per_pair": 12 * spec.members,
+                "ncu": ncu_ctx,
+                "note": "the cell k-NN executes ~1 % of the n(n-1) comparisons at ~7 ALU ops each in SIMT "
+                        "lockstep; the ALU pipe utilisation (ncu) is the hardware-side efficiency"}
     # the same kernel with the sweep disabled (CORR_F_KSG_DENSE): all n(n-1) comparisons executed,
     # results bit-identical -- the ALU-efficiency reference for the dense k-NN pass
     roofline_dense = None
@@ -400,23 +426,19 @@ def main():
                               "pairs_per_s": my_pairs / (stage_ms["pearson_sampled"] / 1e3),
                               "ms_per_step": stage_ms["pearson_sampled"]}
 
-    # e2e: same metric from HOST memory through the C ABI.  Every step uploads its field (7.04 GB
-    # member-major fp32 from pinned host memory; rank 0, then an NCCL broadcast on a separate
-    # communicator), re-ingests it (corr_field_update: transpose, fp64 stats, tf32 split, sorted
-    # rows) and reads its maxima back to pinned host memory.  Two field slots double-buffer the
-    # stream: step i+1's upload + ingest run on a side stream while step i computes.
+    # e2e: same metric from HOST memory through the C ABI.  Every step passes the pinned host field
+    # (7.04 GB member-major fp32) to corr_field_update, which streams it to the device itself
+    # (32-member slices, one cudaMemcpyAsync each, on the field's copy stream, each slice transposed
+    # as it lands) and rebuilds the derived buffers; the step runs and its maxima are read back to
+    # pinned host memory.  Two field slots double-buffer: step i+1's update is issued on a side
+    # stream while step i computes.  Every rank streams its own full replica over its own link.
     e2e = None
     if not args.no_e2e:
-        # each rank holds (pinned) and uploads only its 1/world of the member rows; the
-        # slices are exchanged over NCCL (dist.replicate_field_sharded)
-        mlo, mhi = cdist.member_bounds(spec.members, world)[rank]
-        host = torch.empty((mhi - mlo, spec.points), dtype=torch.float32, pin_memory=True)
-        host.copy_(vals[mlo:mhi])
-        bgroup = tdist.new_group(list(range(world))) if world > 1 else None
-        bufs = [vals, torch.empty_like(vals)]
-        slots = [field, cb.corr_field_create(bufs[1], spec.nx, spec.ny, spec.nz, spec.members, device=local)]
+        host = torch.empty((spec.members, spec.points), dtype=torch.float32, pin_memory=True)
+        host.copy_(vals)
+        slots = [field, cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members, device=local)]
         up = torch.cuda.Stream()
-        h2d = (mhi - mlo) * spec.points * 4  # this rank's slice; the line reports the sum over ranks
+        h2d = spec.members * spec.points * 4
         d2h_holder = [0]
         pinned_out = None
 
@@ -424,8 +446,7 @@ def main():
             with torch.cuda.stream(up):
                 if after is not None:
                     up.wait_event(after)
-                cdist.replicate_field_sharded(host, bufs[slot], rank, world, group=bgroup)
-                cb.corr_field_update(slots[slot], bufs[slot], stream=up)
+                cb.corr_field_update(slots[slot], host.data_ptr(), stream=up)  # HOST pointer
 
         step_evs = []
 
@@ -457,8 +478,8 @@ def main():
         if world > 1:
             tdist.barrier()
         torch.cuda.synchronize()
-        # at least 6 steps: the first step's upload + ingest is the pipeline fill (not overlapped),
-        # later uploads overlap the previous step's compute
+        # at least 6 steps: the first step's update is the pipeline fill (not overlapped), later
+        # updates overlap the previous step's compute
         ne = max(6, args.steps)
         e2e_clocks = ClockSampler(local)
         e2e_clocks.start()
@@ -466,29 +487,29 @@ def main():
         run_e2e(ne)
         e_s = (time.perf_counter() - te) / ne
         e2e_clk = e2e_clocks.stop()
+        for s_ in slots:
+            cb.corr_check(s_)
         if world > 1:
             tt = torch.tensor([e_s], dtype=torch.float64, device=f"cuda:{local}")
             tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
             e_s = float(tt[0])
-            hb = torch.tensor([h2d], dtype=torch.int64, device=f"cuda:{local}")
-            tdist.all_reduce(hb, op=tdist.ReduceOp.SUM)
-            h2d = int(hb[0])
-        e2e = {"value": total_pairs / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": total_pairs / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": d2h_holder[0], "s_per_step": e_s,
                "device_step_ms": [round(a.elapsed_time(b), 1) for a, b in step_evs],
                "clocks": e2e_clk,
-               "includes": "per step: pinned-host upload of the 7.04 GB field (1/N of the member rows per "
-                            "rank, exchanged by NCCL broadcasts), "
-                           "corr_field_update ingest, the step, D2H of the maxima; double-buffered "
-                           "(next field's upload/ingest overlaps the current step)"}
+               "includes": "per step and rank: corr_field_update(pinned HOST pointer of the 7.04 GB field) -- "
+                           "the library streams it (32-member slices, cudaMemcpyAsync on its copy stream) and "
+                           "re-ingests -- then the step and the D2H of the maxima; double-buffered (the next "
+                           "field's update overlaps the current step)"}
         slots[1].close()
+        del host
 
     cpu_base = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         v, dt, _, threads = oracle_sample_run(spec, A, B, S, args.cpu_pairs, SEED)
         cpu_base = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                     "sample": f"first {args.cpu_pairs} sampled pairs of the C4 context view (n=1000, k=3), "
-                              f"oracle.eval_pairs, {dt:.1f} s"}
+                              f"oracle.eval_pairs, {dt:.1f} s on rank 0's host"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -497,6 +518,13 @@ def main():
                 "roofline": roofline, "roofline_ksg_dense": roofline_dense, "roofline_pearson_block": roofline_block,
                 "roofline_pearson_pairs": roofline_pearson_pairs, "cpu_baseline": cpu_base, "e2e": e2e, "clocks": clk,
                 "gpu_launches": launches, "field_create_s": create_s,
+                "ingest": {"bound": "hbm", "kernels": "transpose_kernel + stats_kernel + sort_radix_kernel",
+                           "ms": ing_ms, "bytes": sum(ing_bytes.values()), "bytes_by_kernel": ing_bytes,
+                           "achieved": sum(ing_bytes.values()) / (ing_ms / 1e3) / 1e9, "unit": "GB/s",
+                           "peak": peaks.get("hbm_gbs") or 6552.3,
+                           "frac": sum(ing_bytes.values()) / (ing_ms / 1e3) / 1e9 / (peaks.get("hbm_gbs") or 6552.3),
+                           "note": "algorithmic bytes (each input read once, each plane written once); the "
+                                   "per-kernel split of the time is in the ncu launch list (profiles/)"},
                 "region_max_sample": [float(res[0][0]), int(res[1][0][0]), int(res[1][0][1])]}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -46,13 +46,16 @@ enum { CORR_PEARSON = 0, CORR_KSG = 1 };
 enum {
   CORR_F_KSG_PLUS1 = 1 << 8, /* KSG with psi(n_x+1), psi(n_y+1) (Kraskov alg. 1; reading R1) */
   CORR_F_ABS = 1 << 9,       /* region max of |value| (reading R11)           */
-  CORR_F_KSG_DENSE = 1 << 10 /* KSG: evaluate all n(n-1) comparisons (no exact sweep); same results */
+  CORR_F_KSG_DENSE = 1 << 10, /* KSG: evaluate all n(n-1) comparisons (no pruning); same results  */
+  CORR_F_KSG_COUNT = 1 << 11  /* KSG: tally executed comparisons for corr_ksg_comparisons (slower; */
+                              /* same results) -- a diagnostic for the roofline report          */
 };
 enum { CORR_OK = 0, CORR_E_INVAL = -1, CORR_E_RANGE = -2, CORR_E_NOMEM = -3, CORR_E_CUDA = -4 };
 
 /* corr_field_create -- ingest one variable of an ensemble.
  *   values   : float32 [members][nz][ny][nx] (the paper's/SPEC's file order),
- *              host or device pointer (detected); copied, caller keeps ownership.
+ *              host or device pointer (detected); copied, caller keeps ownership.  A host
+ *              pointer is streamed in 32-member slices as in corr_field_update.
  *   nx,ny,nz : grid dims >= 1;  2 <= members (n) <= 4096 (a pair is staged in shared memory).
  *   device   : CUDA ordinal the field lives on; the call makes it current.
  * Builds, on `device`: member-contiguous rows F[P][n_pad] (n_pad = ceil(n/8)*8),
@@ -78,10 +81,16 @@ int corr_field_aggregate(const corr_field* f, int32_t fx, int32_t fy, int32_t fz
 /* corr_field_update -- replace the member values of an existing field (same dims and members;
  * e.g. the next forecast time of the ensemble) and rebuild every derived buffer in place, with no
  * device allocation.  values: float32 [members][nz][ny][nx], host or device.
- * Work is ordered on `cuda_stream`, which is synchronised (validation); calls on other streams that
- * still read the field must be ordered before it by the caller (events).  Errors: CORR_E_INVAL
- * (non-finite value; the field content is then undefined until the next successful update),
- * CORR_E_NOMEM (host input staging), CORR_E_CUDA. */
+ * Asynchronous on `cuda_stream` (no host synchronisation).  A HOST pointer is streamed by the
+ * library: slices of 32 member rows (contiguous in the input) are copied with one
+ * cudaMemcpyAsync each on the field's own copy stream into two persistent device slices (allocated
+ * on the first host update, 2 x 32 x P x 4 bytes) and each slice is transposed on `cuda_stream` as
+ * soon as it has landed; page-locked (pinned) memory makes the copies overlap device work.  The
+ * host buffer must stay unchanged until `cuda_stream` has passed this call's work.  Calls on
+ * other streams that still read the field must be ordered before it by the caller (events).
+ * A non-finite value is detected on the device: the next corr_check() returns CORR_E_INVAL (the
+ * field content is undefined until the next clean update).
+ * Errors (immediate): CORR_E_INVAL (NULL arguments), CORR_E_NOMEM (staging), CORR_E_CUDA. */
 int corr_field_update(corr_field* f, const float* values, void* cuda_stream);
 
 /* Frees the field's device memory (device-synchronising).  NULL is a no-op. */
@@ -142,15 +151,17 @@ int corr_ksg_debug(const corr_field* fa, const corr_field* fb, int32_t k, const 
                    const int64_t* idxB, int64_t npairs, float* eps, int32_t* nx, int32_t* ny,
                    void* cuda_stream);
 
-/* corr_check -- synchronises `cuda_stream`; returns CORR_E_RANGE (and clears the flag)
- * if an earlier call on `f`'s device saw an out-of-range point index, CORR_E_CUDA on a
- * CUDA error, else CORR_OK. */
+/* corr_check -- synchronises `cuda_stream`; returns CORR_E_INVAL if an earlier
+ * corr_field_update of `f` saw a non-finite input value, CORR_E_RANGE if an earlier call on
+ * `f`'s device saw an out-of-range point index (either flag is cleared when reported),
+ * CORR_E_CUDA on a CUDA error, else CORR_OK. */
 int corr_check(const corr_field* f, void* cuda_stream);
 
 /* corr_ksg_comparisons -- KSG member-comparisons (d_ij evaluations) executed on
- * `device` since the last reset; the exact sweep skips comparisons that provably cannot change
- * any eps_i, so this is <= n(n-1) per pair.  Synchronises the device; reset != 0 zeroes the
- * counter after reading.  Diagnostic for the roofline report (bench.py). */
+ * `device` since the last reset; the pruned k-NN passes skip comparisons that provably cannot
+ * change any eps_i, so this is <= n(n-1) per pair.  The default column-cell kernel (n >= 128,
+ * k <= 8) counts only in calls with CORR_F_KSG_COUNT.  Synchronises the device; reset != 0 zeroes
+ * the counter after reading.  Diagnostic for the roofline report (bench.py). */
 int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset);
 
 /* corr_gemm_flops -- tensor-core work executed on `device` by the exhaustive Pearson block path

@@ -49,6 +49,12 @@ struct DeviceGuard {
 
 void free_field(corr_field* f) {
   if (!f) return;
+  for (int i = 0; i < 2; ++i) {
+    if (f->stage[i]) cudaFree(f->stage[i]);
+    if (f->ev_copied[i]) cudaEventDestroy(f->ev_copied[i]);
+    if (f->ev_used[i]) cudaEventDestroy(f->ev_used[i]);
+  }
+  if (f->copy_st) cudaStreamDestroy(f->copy_st);
   cudaFree(f->F);
   cudaFree(f->Z);
   cudaFree(f->Zhi);
@@ -121,19 +127,35 @@ int alloc_field(int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t dev
 bool ksg_plus1(int32_t measure) { return (measure & CORR_F_KSG_PLUS1) != 0; }
 KsgPath ksg_path(int32_t measure) { return (measure & CORR_F_KSG_DENSE) ? kKsgDense : kKsgAuto; }
 
-// Copies member-major values (host or device) into f and rebuilds every derived buffer on `st`;
-// synchronises `st` (input validation).  The non-finite flag lives in err[1], the index-range
-// flag of corr_check in err[0].
-int ingest_values(corr_field* f, const float* values, cudaStream_t st, const char* who) {
-  auto alloc = [&](void** p, size_t bytes) -> bool {
-    if (cudaMalloc(p, bytes) != cudaSuccess) {
+// Host-input staging of a field: two device slices of kStageMembers members each, a copy stream
+// and the events ordering copies against transposes.  Created on the first host upload, kept for
+// the field's lifetime (corr_field_update streams without allocating).
+int ensure_staging(corr_field* f) {
+  if (f->stage[0]) return CORR_OK;
+  const size_t bytes = (size_t)kStageMembers * (size_t)f->P * 4;
+  for (int i = 0; i < 2; ++i) {
+    if (cudaMalloc((void**)&f->stage[i], bytes) != cudaSuccess) {
       cudaGetLastError();
-      return false;
+      return fail(CORR_E_NOMEM, "device allocation failed for the host-upload staging slices");
     }
-    return true;
-  };
-  const float* dvalues = values;
-  float* staging = nullptr;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&f->copy_st, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&f->ev_copied[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_used[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "host-upload staging");
+  return CORR_OK;
+}
+
+// Copies member-major values (host or device) into f and rebuilds every derived buffer on `st`.
+// Host input is streamed: member slices of kStageMembers rows (contiguous in the [n][P] input,
+// one cudaMemcpyAsync each) alternate between two device slices on the field's copy stream, and
+// each slice is transposed into F on `st` as soon as it has landed, so the PCIe transfer overlaps
+// the transposes (and, with pinned memory, whatever else runs on the device).  Non-finite values
+// set err[1] bit 1 on the device; `sync` (corr_field_create) waits and reports them, otherwise
+// (corr_field_update) the call returns at once and corr_check() reports them.
+int ingest_values(corr_field* f, const float* values, cudaStream_t st, const char* who, bool sync) {
   cudaPointerAttributes attr;
   memset(&attr, 0, sizeof(attr));
   const cudaError_t pe = cudaPointerGetAttributes(&attr, values);
@@ -142,17 +164,32 @@ int ingest_values(corr_field* f, const float* values, cudaStream_t st, const cha
                          (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
                          attr.device == f->device;
   cudaError_t e = cudaMemsetAsync(f->err + 1, 0, sizeof(int), st);
-  if (e == cudaSuccess && !on_device) {
-    const size_t bytes = (size_t)f->n * (size_t)f->P * 4;
-    if (!alloc((void**)&staging, bytes)) return fail(CORR_E_NOMEM, "device allocation failed for the input staging buffer");
-    e = cudaMemcpyAsync(staging, values, bytes, cudaMemcpyHostToDevice, st);
-    dvalues = staging;
+  if (e == cudaSuccess && on_device) {
+    e = launch_field_ingest(f, values, st);
+  } else if (e == cudaSuccess) {
+    const int rc = ensure_staging(f);
+    if (rc) return rc;
+    const size_t slice = (size_t)f->P * 4;  // bytes of one member row of the input
+    for (int m0 = 0, i = 0; m0 < f->n && e == cudaSuccess; m0 += kStageMembers, ++i) {
+      const int m1 = m0 + kStageMembers < f->n ? m0 + kStageMembers : f->n;
+      const int b = i & 1;
+      // the slice buffer is free once the transpose that last read it has run
+      e = cudaStreamWaitEvent(f->copy_st, f->ev_used[b], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(f->stage[b], values + (size_t)m0 * f->P, (size_t)(m1 - m0) * slice,
+                            cudaMemcpyHostToDevice, f->copy_st);
+      if (e == cudaSuccess) e = cudaEventRecord(f->ev_copied[b], f->copy_st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, f->ev_copied[b], 0);
+      if (e == cudaSuccess) e = launch_transpose_slice(f, f->stage[b], m0, m1, st);
+      if (e == cudaSuccess) e = cudaEventRecord(f->ev_used[b], st);
+    }
+    if (e == cudaSuccess) e = launch_field_ingest(f, nullptr, st);
   }
-  if (e == cudaSuccess) e = launch_field_ingest(f, dvalues, st);
+  if (e != cudaSuccess) return cuda_fail(e, who);
+  if (!sync) return CORR_OK;
   int herr = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, f->err + 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+  e = cudaMemcpyAsync(&herr, f->err + 1, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (staging) cudaFree(staging);
   if (e != cudaSuccess) return cuda_fail(e, who);
   if (herr & 2) return fail(CORR_E_INVAL, "non-finite input value (SPEC.md:72)");
   return CORR_OK;
@@ -169,7 +206,8 @@ int check_pair_fields(const corr_field* fa, const corr_field*& fb) {
 int resolve_k(const corr_field* f, int32_t measure, int32_t& k) {
   const int kind = measure & 0xFF;
   if (kind != CORR_PEARSON && kind != CORR_KSG) return fail(CORR_E_INVAL, "unknown measure kind");
-  if (measure & ~(0xFF | CORR_F_KSG_PLUS1 | CORR_F_ABS | CORR_F_KSG_DENSE)) return fail(CORR_E_INVAL, "unknown measure flags");
+  if (measure & ~(0xFF | CORR_F_KSG_PLUS1 | CORR_F_ABS | CORR_F_KSG_DENSE | CORR_F_KSG_COUNT))
+    return fail(CORR_E_INVAL, "unknown measure flags");
   if (kind == CORR_PEARSON) {
     k = 0;
     return CORR_OK;
@@ -294,7 +332,7 @@ int corr_field_create(const float* values, int32_t nx, int32_t ny, int32_t nz, i
   corr_field* f = nullptr;
   const int arc = alloc_field(nx, ny, nz, members, device, st, &f);
   if (arc) return arc;
-  const int rc = ingest_values(f, values, st, "corr_field_create");
+  const int rc = ingest_values(f, values, st, "corr_field_create", true);
   if (rc) {
     free_field(f);
     return rc;
@@ -308,7 +346,7 @@ int corr_field_update(corr_field* f, const float* values, void* cuda_stream) {
   if (!values) return fail(CORR_E_INVAL, "values is NULL");
   DeviceGuard guard(f->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
-  return ingest_values(f, values, (cudaStream_t)cuda_stream, "corr_field_update");
+  return ingest_values(f, values, (cudaStream_t)cuda_stream, "corr_field_update", false);
 }
 
 int corr_field_aggregate(const corr_field* f, int32_t fx, int32_t fy, int32_t fz, void* cuda_stream,
@@ -384,7 +422,7 @@ static int eval_pairs_impl(const corr_field* fa, const corr_field* fb, int32_t m
   cudaStream_t st = (cudaStream_t)cuda_stream;
   cudaError_t e;
   if ((measure & 0xFF) == CORR_KSG) {
-    e = launch_ksg(fa, fb, k, ksg_plus1(measure), ksg_path(measure), src, po, st);
+    e = launch_ksg(fa, fb, k, ksg_plus1(measure), ksg_path(measure), (measure & CORR_F_KSG_COUNT) != 0, src, po, st);
     if (e == cudaErrorNotSupported) return fail(CORR_E_INVAL, "KSG with k > 32 is not supported");
   } else {
     e = launch_pearson_pairs(fa, fb, src, po, st);
@@ -481,7 +519,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
   po.absval = (measure & CORR_F_ABS) != 0;
   if (e == cudaSuccess) {
     if ((measure & 0xFF) == CORR_KSG) {
-      e = launch_ksg(fa, fb, k, ksg_plus1(measure), ksg_path(measure), src, po, st);
+      e = launch_ksg(fa, fb, k, ksg_plus1(measure), ksg_path(measure), (measure & CORR_F_KSG_COUNT) != 0, src, po, st);
       if (e == cudaErrorNotSupported) {
         if (own_reg) cudaFreeAsync(dreg, st);
         cudaFreeAsync(keys, st);
@@ -512,10 +550,15 @@ int corr_check(const corr_field* f, void* cuda_stream) {
   cudaError_t e = cudaStreamSynchronize(st);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "corr_check");
-  int h = 0;
-  e = cudaMemcpy(&h, f->err, sizeof(int), cudaMemcpyDeviceToHost);
+  int h[2] = {0, 0};
+  e = cudaMemcpy(h, f->err, sizeof(h), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "corr_check");
-  if (h & 1) {
+  if (h[1] & 2) {
+    const int zero = 0;
+    cudaMemcpy(f->err + 1, &zero, sizeof(int), cudaMemcpyHostToDevice);
+    return fail(CORR_E_INVAL, "non-finite input value in an earlier corr_field_update (SPEC.md:72)");
+  }
+  if (h[0] & 1) {
     const int zero = 0;
     cudaMemcpy(f->err, &zero, sizeof(int), cudaMemcpyHostToDevice);
     return fail(CORR_E_RANGE, "point index out of range in an earlier call");

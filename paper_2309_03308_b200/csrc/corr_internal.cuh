@@ -26,6 +26,11 @@ struct corr_field {
   double* psi;    // [n + 2] digamma at integers, psi[0] = NaN
   int* err;       // device status words: err[0] bit0 = index out of range, err[1] bit1 = non-finite input
   void* tmaps;    // lazily built TMA descriptors (pearson_gemm.cu)
+  // host-input streaming (api.cu ingest_values): two device slices of kStageMembers members,
+  // a copy stream and the events that order copies against the transposes (lazily created)
+  float* stage[2];
+  cudaStream_t copy_st;
+  cudaEvent_t ev_copied[2], ev_used[2];
 };
 
 #include <atomic>
@@ -71,6 +76,8 @@ struct PairOut {
 
 // ---- launchers (defined in the .cu files) ----
 cudaError_t launch_field_ingest(corr_field* f, const float* dvalues_member_major, cudaStream_t st);
+cudaError_t launch_transpose_slice(corr_field* f, const float* dslice, int m0, int m1, cudaStream_t st);
+constexpr int kStageMembers = 32;  // members per host-upload slice (one transpose tile row)
 cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int fx, int fy, int fz, cudaStream_t st);
 // Which k-NN formulation launch_ksg runs (all give bit-identical eps / counts / MI):
 //   kKsgAuto  -- column-cell kernel for 128 <= n, k <= 8 (ksg_cell.cu), else the sweep / warp /
@@ -78,10 +85,12 @@ cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int f
 //   kKsgDense -- every n(n-1) comparison (CORR_F_KSG_DENSE);
 //   kKsgSweep -- the round-1 x-sorted exact sweep (A/B reference; env CORR_KSG_PATH=sweep).
 enum KsgPath { kKsgAuto = 0, kKsgDense = 1, kKsgSweep = 2 };
-cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool plus1, KsgPath path,
+// count: tally executed comparisons (corr_ksg_comparisons) -- the column-cell kernel does so only
+// when asked (CORR_F_KSG_COUNT), the ksg.cu kernels always.
+cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool plus1, KsgPath path, bool count,
                        const PairSrc& src, const PairOut& out, cudaStream_t st);
-cudaError_t launch_ksg_cell(const corr_field* fa, const corr_field* fb, int k, bool plus1, const PairSrc& src,
-                            const PairOut& out, cudaStream_t st);
+cudaError_t launch_ksg_cell(const corr_field* fa, const corr_field* fb, int k, bool plus1, bool count,
+                            const PairSrc& src, const PairOut& out, cudaStream_t st);
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset);
 // Device copy of a small host table (region lists) that stays resident and is reused when the
 // same bytes come again: no host->device copy on the call path of repeated calls.  (A small copy

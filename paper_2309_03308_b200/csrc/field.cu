@@ -24,20 +24,23 @@ namespace corr {
 namespace {
 
 // ---- 1. transpose [n][P] -> F[P][n_pad] through a 32x32 shared tile -----------
+// `in` holds members [m0, m1) of the member-major input ([m1-m0][P]); the kernel writes columns
+// [m0, m0 + mw) of F (mw extends to n_pad on the last slice: pad columns are written as 0), so the
+// host path can stream the input in member slices and transpose each as soon as it lands.
 __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict__ in, float* __restrict__ F,
-                                                        int n, int n_pad, int64_t P, int* err) {
+                                                        int m0, int m1, int mw, int n_pad, int64_t P, int* err) {
   __shared__ float tile[32][33];
   const int64_t p0 = (int64_t)blockIdx.x * 32;
-  const int m0 = blockIdx.y * 32;
+  const int mb = m0 + blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   bool bad = false;
 #pragma unroll
   for (int r = 0; r < 32; r += 8) {
-    const int m = m0 + ty + r;
+    const int m = mb + ty + r;
     const int64_t p = p0 + tx;
     float v = 0.f;
-    if (m < n && p < P) {
-      v = in[(int64_t)m * P + p];
+    if (m < m1 && p < P) {
+      v = in[(int64_t)(m - m0) * P + p];
       bad |= !isfinite(v);
     }
     tile[ty + r][tx] = v;
@@ -47,8 +50,8 @@ __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict_
 #pragma unroll
   for (int r = 0; r < 32; r += 8) {
     const int64_t p = p0 + ty + r;
-    const int m = m0 + tx;
-    if (p < P && m < n_pad) F[p * n_pad + m] = tile[tx][ty + r];
+    const int m = mb + tx;
+    if (p < P && m < m0 + mw) F[p * n_pad + m] = tile[tx][ty + r];
   }
 }
 
@@ -280,13 +283,22 @@ cudaError_t launch_field_aggregate(const corr_field* src, corr_field* dst, int f
   return launch_field_ingest(dst, nullptr, st);
 }
 
-// din == nullptr: F is already filled (aggregate levels); else transpose din [n][P] into F.
+// Transposes members [m0, m1) of the member-major input (din = that slice, [m1-m0][P]) into F.
+cudaError_t launch_transpose_slice(corr_field* f, const float* din, int m0, int m1, cudaStream_t st) {
+  const int mw = (m1 >= f->n ? f->n_pad : m1) - m0;
+  dim3 grid((unsigned)((f->P + 31) / 32), (unsigned)((mw + 31) / 32));
+  transpose_kernel<<<grid, 256, 0, st>>>(din, f->F, m0, m1, mw, f->n_pad, f->P, f->err + 1);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// din == nullptr: F is already filled (aggregate levels, or a streamed host upload); else
+// transpose din [n][P] into F.  Then the derived buffers (stats, tf32/bf16 planes, sorted rows).
 cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st) {
   const int64_t P = f->P;
   if (din) {
-    dim3 grid((unsigned)((P + 31) / 32), (unsigned)((f->n_pad + 31) / 32));
-    transpose_kernel<<<grid, 256, 0, st>>>(din, f->F, f->n, f->n_pad, P, f->err + 1);
-    note_launch();
+    const cudaError_t e = launch_transpose_slice(f, din, 0, f->n, st);
+    if (e != cudaSuccess) return e;
   }
   {
     const int64_t threads = P * 32;

@@ -866,7 +866,7 @@ cudaError_t launch_k(const corr_field* fa, const corr_field* fb, int k, int plus
 
 }  // namespace
 
-cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool plus1_flag, KsgPath path,
+cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool plus1_flag, KsgPath path, bool count,
                        const PairSrc& src, const PairOut& out, cudaStream_t st) {
   if (src.nunits == 0) return cudaSuccess;
   static const bool env_sweep = [] {
@@ -874,7 +874,7 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool p
     return v && v[0] == 's';
   }();
   if (path == kKsgAuto && env_sweep) path = kKsgSweep;
-  if (path == kKsgAuto && fa->n > kWarpKernelMaxN && k <= 8) return launch_ksg_cell(fa, fb, k, plus1_flag, src, out, st);
+  if (path == kKsgAuto && fa->n > kWarpKernelMaxN && k <= 8) return launch_ksg_cell(fa, fb, k, plus1_flag, count, src, out, st);
   // internal plumbing of the ksg.cu launchers: bit 0 = psi(n+1) variant, bit 1 = dense
   const int plus1 = (plus1_flag ? 1 : 0) | (path == kKsgDense ? 2 : 0);
   switch (k) {

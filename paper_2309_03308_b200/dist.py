@@ -72,30 +72,6 @@ def gather_region_results(out_max: torch.Tensor, out_arg: torch.Tensor, bounds: 
     return full_max, full_arg
 
 
-def member_bounds(members: int, world: int) -> List[Tuple[int, int]]:
-    """Contiguous member-row slices [lo, hi) of a [members][points] field, one per rank."""
-    return [(members * r // world, members * (r + 1) // world) for r in range(world)]
-
-
-def replicate_field_sharded(host_slice: torch.Tensor, out: torch.Tensor, rank: int, world: int, group=None) -> int:
-    """Builds a full field replica on every rank from 1/world of it per rank.
-
-    Rank r copies ITS member rows (``host_slice``, pinned host memory, rows
-    member_bounds()[r]) into ``out[lo:hi]`` over its own PCIe link, then every rank
-    broadcasts its slice to the others (NVLink/NVSwitch under NCCL).  Each GPU thus
-    receives 1/world of the field from the host instead of rank 0 uploading all of it.
-    Returns the host->device bytes this rank copied."""
-    bounds = member_bounds(out.shape[0], world)
-    lo, hi = bounds[rank]
-    if hi > lo:
-        out[lo:hi].copy_(host_slice, non_blocking=True)
-    if world > 1:
-        for r, (a, b) in enumerate(bounds):
-            if b > a:
-                tdist.broadcast(out[a:b], r, group=group)
-    return (hi - lo) * out.shape[1] * out.element_size()
-
-
 def split_box_z(box, world: int):
     """Split one region box into `world` slabs along its longest axis (focus view, one
     region pair: SURVEY.md §8(e) "C2 ... split A into R row slabs")."""
@@ -136,3 +112,66 @@ def combine_focus(maxes: Sequence[float], args: Sequence[Tuple[int, int]], slabs
     if best is None:
         return float("nan"), (-1, -1)
     return best[0], (best[2], best[3])
+
+
+_MASK32 = 0xFFFFFFFF
+_TOP = -(1 << 63)  # int64 with only the sign bit: maps unsigned key order onto signed order
+
+
+def focus_key(fm: torch.Tensor, fa: torch.Tensor, slabs, boxB, nx: int, ny: int) -> torch.Tensor:
+    """Order-preserving int64 key of one rank's focus-slab maximum (on the tensors' device):
+    the orderable bits of the fp32 value (reading R16: NaN never wins, -0 == +0) above
+    0xFFFFFFFF - q, with q = a_local*|B| + b_local in the FULL box A (the union of the slabs), so
+    the larger key is the larger value and, among equal values, the lower q; a slab without a
+    defined value gets the smallest key."""
+    fx0, fy0, fz0 = min(s_[0] for s_ in slabs), min(s_[1] for s_ in slabs), min(s_[2] for s_ in slabs)
+    fx1, fy1 = max(s_[3] for s_ in slabs), max(s_[4] for s_ in slabs)
+    ax, ay = fx1 - fx0, fy1 - fy0
+    bx, by = boxB[3] - boxB[0], boxB[4] - boxB[1]
+    nB = bx * by * (boxB[5] - boxB[2])
+    a, b = fa.reshape(-1, 2)[:, 0], fa.reshape(-1, 2)[:, 1]
+    xa, ya, za = a % nx, (a // nx) % ny, a // (nx * ny)
+    xb, yb, zb = b % nx, (b // nx) % ny, b // (nx * ny)
+    q = (((za - fz0) * ay + (ya - fy0)) * ax + (xa - fx0)) * nB + ((zb - boxB[2]) * by + (yb - boxB[1])) * bx + (xb - boxB[0])
+    v = fm.reshape(-1).to(torch.float32) + 0.0
+    u = v.view(torch.int32).to(torch.int64) & _MASK32
+    u = torch.where((u >> 31) == 1, u ^ _MASK32, u ^ 0x80000000)
+    key = ((u << 32) | (_MASK32 - q)) ^ _TOP
+    bad = torch.isnan(v) | (a < 0)
+    return torch.where(bad, torch.full_like(key, _TOP), key)
+
+
+def decode_focus_key(key: torch.Tensor, slabs, boxB, nx: int, ny: int):
+    """Inverse of focus_key: (value float32 [m], argmax int64 [m, 2]); the smallest key ->
+    (nan, (-1, -1))."""
+    fx0, fy0, fz0 = min(s_[0] for s_ in slabs), min(s_[1] for s_ in slabs), min(s_[2] for s_ in slabs)
+    fx1, fy1 = max(s_[3] for s_ in slabs), max(s_[4] for s_ in slabs)
+    ax, ay = fx1 - fx0, fy1 - fy0
+    bx, by = boxB[3] - boxB[0], boxB[4] - boxB[1]
+    nB = bx * by * (boxB[5] - boxB[2])
+    k = key ^ _TOP
+    u = (k >> 32) & _MASK32
+    q = _MASK32 - (k & _MASK32)
+    u = torch.where((u >> 31) == 1, u ^ 0x80000000, u ^ _MASK32)
+    v = (u - ((u >> 31) << 32)).to(torch.int32).view(torch.float32)  # low 32 bits as int32
+    al, bl = q // nB, q % nB
+    a = ((fz0 + al // (ax * ay)) * ny + (fy0 + (al // ax) % ay)) * nx + (fx0 + al % ax)
+    b = ((boxB[2] + bl // (bx * by)) * ny + (boxB[1] + (bl // bx) % by)) * nx + (boxB[0] + bl % bx)
+    none = key == _TOP
+    v = torch.where(none, torch.full_like(v, float("nan")), v)
+    arg = torch.stack([torch.where(none, torch.full_like(a, -1), a), torch.where(none, torch.full_like(b, -1), b)], -1)
+    return v, arg
+
+
+def combine_focus_device(fm: torch.Tensor, fa: torch.Tensor, slabs, boxB, nx: int, ny: int, group=None):
+    """Combines the ranks' focus-slab maxima of ONE region pair with a single all-reduce MAX over
+    the packed keys ("all-reduce MAX on the packed u64 key"), on the device under
+    NCCL; same result as combine_focus (max value, ties -> lowest q in the full box A)."""
+    key = focus_key(fm, fa, slabs, boxB, nx, ny)
+    if key.is_cuda and tdist.get_backend(group) == "gloo":
+        host = key.cpu()
+        tdist.all_reduce(host, op=tdist.ReduceOp.MAX, group=group)
+        key.copy_(host)
+    else:
+        tdist.all_reduce(key, op=tdist.ReduceOp.MAX, group=group)
+    return decode_focus_key(key, slabs, boxB, nx, ny)

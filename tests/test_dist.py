@@ -55,6 +55,10 @@ def _worker(rank, world, port, q):
     parts = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
     tdist.all_gather(parts, torch.tensor([sm[0], sa[0][0], sa[0][1]], dtype=torch.float64))
     v, ab = cdist.combine_focus([float(p[0]) for p in parts], [(int(p[1]), int(p[2])) for p in parts], slabs, FB, 8, 8)
+    # the same combine as ONE all-reduce MAX over packed keys (the device path of bench.py)
+    dv, dab = cdist.combine_focus_device(torch.tensor([sm[0]], dtype=torch.float32), torch.tensor(sa),
+                                         slabs, FB, 8, 8)
+    assert float(dv[0]) == np.float32(v) and tuple(int(t) for t in dab[0]) == tuple(ab)
     q.put((rank, fm.numpy(), fa.numpy(), v, ab))
     tdist.barrier()
     tdist.destroy_process_group()
@@ -84,33 +88,24 @@ def test_gloo_shards_gather_bit_identical(world):
         assert v == fm_ref[0] and tuple(ab) == tuple(fa_ref[0])
 
 
-def _repl_worker(rank, world, port, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    tdist.init_process_group("gloo", rank=rank, world_size=world)
-    spec = synth.spec_of(synth.C1)
-    full = synth.generate(spec)                      # [members][points]; every rank knows only its slice
-    lo, hi = cdist.member_bounds(spec.members, world)[rank]
-    out = torch.full_like(full, float("nan"))
-    nbytes = cdist.replicate_field_sharded(full[lo:hi].clone(), out, rank, world)
-    q.put((rank, bool(torch.equal(out, full)), nbytes))
-    tdist.barrier()
-    tdist.destroy_process_group()
-
-
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_sharded_field_replication(world):
-    """Each rank uploads 1/world of the member rows; the broadcasts rebuild the full replica
-    bit for bit on every rank (bench.py e2e at N > 1)."""
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_repl_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    spec = synth.spec_of(synth.C1)
-    assert all(ok for _, ok, _ in res)
-    assert sum(b for _, _, b in res) == spec.members * spec.points * 4
+def test_focus_key_order_and_roundtrip():
+    """Packed focus keys: larger value wins, equal values -> lower q in the full box A, NaN /
+    missing never wins, -0 == +0; decode inverts encode."""
+    slabs = cdist.split_box_z((0, 0, 0, 8, 8, 4), 3)
+    boxB = (0, 0, 0, 4, 4, 2)
+    nx, ny = 8, 8
+    vals = torch.tensor([0.5, 0.5, -0.0, 0.0, float("nan"), -1.0, 0.75], dtype=torch.float32)
+    pa = [(3 * 64 + 2 * 8 + 1), (0 * 64 + 1), 5, 6, 7, 8, 2 * 64]
+    pb = [9, 9, 1, 2, 3, 8, 0]  # inside boxB
+    fa = torch.tensor(list(zip(pa, pb)), dtype=torch.int64)
+    keys = cdist.focus_key(vals, fa, slabs, boxB, nx, ny)
+    v, arg = cdist.decode_focus_key(keys, slabs, boxB, nx, ny)
+    ok = ~torch.isnan(vals)
+    assert torch.equal(v[ok], vals[ok] + 0.0) and torch.isnan(v[4])
+    assert torch.equal(arg[ok], fa[ok]) and arg[4].tolist() == [-1, -1]
+    assert keys[6] > keys[0] > keys[5] > keys[4]           # value order, NaN lowest
+    assert keys[1] > keys[0]                               # tie -> lower q (a earlier in box A)
+    assert keys[2] > keys[3] or keys[3] > keys[2]          # -0 and +0 compare as equal values ...
+    k0 = cdist.focus_key(torch.tensor([-0.0]), fa[2:3], slabs, boxB, nx, ny)
+    k1 = cdist.focus_key(torch.tensor([0.0]), fa[2:3], slabs, boxB, nx, ny)
+    assert torch.equal(k0, k1)                             # ... same pair: identical keys

@@ -310,9 +310,11 @@ def test_field_update_equals_fresh_create():
         assert torch.equal(m1, m2) and torch.equal(a1, a2)
     bad = v1.clone()
     bad[1, 2] = float("inf")
-    with pytest.raises(cb.CorrError) as e:
-        cb.corr_field_update(f, bad)
-    assert e.value.code == cb.CORR_E_INVAL
+    for src in (bad, bad.cpu().pin_memory()):
+        cb.corr_field_update(f, src)  # asynchronous: the device flag is reported by corr_check
+        with pytest.raises(cb.CorrError) as e:
+            cb.corr_check(f)
+        assert e.value.code == cb.CORR_E_INVAL
     cb.corr_field_update(f, v1)
     cb.corr_check(f)
 
