@@ -105,7 +105,8 @@ int corr_field_info(const corr_field* f, int32_t* nx, int32_t* ny, int32_t* nz,
  *   fa, fb   : fields; fb == NULL means fb = fa (one variable).  fb must match fa's
  *              dims, members and device.
  *   measure  : CORR_PEARSON or CORR_KSG, | flags.
- *   k        : KSG neighbour order, 1 <= k <= n-1; k == 0 selects the paper's
+ *   k        : KSG neighbour order, 1 <= k <= n-1 (every k is supported: register lists for
+ *              k <= 32, multi-pass batched lists above); k == 0 selects the paper's
  *              ceil(3n/100) clamped to [1, n-1].  Ignored for Pearson.
  *              KSG needs n >= 4.
  *   idxA,idxB: DEVICE int64 [npairs] point indices into fa / fb.

@@ -423,7 +423,7 @@ static int eval_pairs_impl(const corr_field* fa, const corr_field* fb, int32_t m
   cudaError_t e;
   if ((measure & 0xFF) == CORR_KSG) {
     e = launch_ksg(fa, fb, k, ksg_plus1(measure), ksg_path(measure), (measure & CORR_F_KSG_COUNT) != 0, src, po, st);
-    if (e == cudaErrorNotSupported) return fail(CORR_E_INVAL, "KSG with k > 32 is not supported");
+    if (e == cudaErrorNotSupported) return fail(CORR_E_INVAL, "KSG configuration not supported");
   } else {
     e = launch_pearson_pairs(fa, fb, src, po, st);
   }
@@ -523,7 +523,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
       if (e == cudaErrorNotSupported) {
         if (own_reg) cudaFreeAsync(dreg, st);
         cudaFreeAsync(keys, st);
-        return fail(CORR_E_INVAL, "KSG with k > 32 is not supported");
+        return fail(CORR_E_INVAL, "KSG configuration not supported");
       }
     } else if (samples == 0) {
       e = launch_pearson_block(fa, fb, reg.data(), dreg, nregion_pairs, po.absval, keys, st);

@@ -463,7 +463,15 @@ __device__ __forceinline__ void batch_merge32(float (&l)[32], float (&d)[32]) {
   }
 }
 
-template <int KT, bool SWEEP>
+// k >= 33 (the paper's k = ceil(3n/100) for n >= 1067): MULTI-PASS batched lists.  Pass p keeps
+// the 32 smallest distances ABOVE a floor (the previous pass's 32nd value; -1 in pass 0) and counts
+// c_p = #{d <= floor} over all j (self included); the (k+1)-th smallest overall is then
+// L_p[k - c_p] as soon as k - c_p < 32 (the multiset below the floor is exactly c_p long, and L_p
+// lists the next values in order -- ties at the floor are all counted, none listed; k - c_p < 0
+// means rank k is one of the floor's unlisted tie copies, eps = floor).  Every pass
+// is a full exact sweep: unvisited or filtered candidates have d >= l[31] > floor, so the count is
+// exact.  Lanes that are done keep their eps; the warp runs passes until every lane is done.
+template <int KT, bool SWEEP, bool MULTI>
 __device__ __forceinline__ int ksg_block_big(const float2* __restrict__ xy, const float* __restrict__ sy, int n,
                                              int nch, int log2p, int mb, int lane, int k,
                                              const double* __restrict__ psi, int off, double& acc,
@@ -472,58 +480,87 @@ __device__ __forceinline__ int ksg_block_big(const float2* __restrict__ xy, cons
   const int ti = mb * 32 + lane;
   const float2 zi = xy[ti];
   float l[32];
-#pragma unroll
-  for (int t = 0; t < 32; ++t) l[t] = INFINITY;
   const float4* xy4 = reinterpret_cast<const float4*>(xy);
   const int c0 = mb, c1 = mb + 1;
-  int ncand = min(32, n - c0 * 32) - 1;
-  // chunk sequence: own block (exact), then below / above alternately; the first chunk in each
-  // direction is merged unconditionally, later ones only if some lane has a candidate < l[KT]
-  int hlo = c0 - 1, hhi = c1, dir = 1;
-  int h = c0;
-  bool exact = true;
+  int ncand = 0;
+  float floor_ = -1.f;  // distances are >= 0: pass 0 has no floor
+  float e = INFINITY;
+  bool done = ti >= n;
 #pragma unroll 1
   while (true) {
-    float d[32];
-    const float4* cp = xy4 + h * 16;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const float4 v = cp[q];
-      d[2 * q] = cheb(zi, make_float2(v.x, v.y));
-      d[2 * q + 1] = cheb(zi, make_float2(v.z, v.w));
-    }
-    bool merge = exact;
-    if (!merge) {
-      float m = d[0];
-#pragma unroll
-      for (int q = 1; q < 32; ++q) m = fminf(m, d[q]);
-      merge = __any_sync(0xffffffffu, m < l[KT]);
-    }
-    if (merge) batch_merge32(l, d);
-    if (h != c0) ncand += min(32, n - h * 32);
-    // next chunk: alternate directions; a direction ends at the array edge or by the sweep test
-    bool found = false;
+    for (int t = 0; t < 32; ++t) l[t] = INFINITY;
+    int below = 0;  // #{d <= floor_} (MULTI)
+    ncand += min(32, n - c0 * 32) - 1;
+    // chunk sequence: own block (exact), then below / above alternately; the first chunk in each
+    // direction is merged unconditionally, later ones only if some lane has a candidate < l[KT]
+    int hlo = c0 - 1, hhi = c1, dir = 1;
+    int h = c0;
+    bool exact = true;
 #pragma unroll 1
-    for (int tries = 0; tries < 2 && !found; ++tries) {
-      dir ^= 1;
-      const int hc = dir ? hhi : hlo;
-      if (dir ? hc >= nch : hc < 0) continue;
-      bool need = true;
-      if (SWEEP) {
-        const float xe = xy[hc * 32 + (dir ? 0 : 31)].x;
-        const float gap = dir ? xe - zi.x : zi.x - xe;
-        need = __any_sync(0xffffffffu, (ti < n) && (gap < l[KT]));
+    while (true) {
+      float d[32];
+      const float4* cp = xy4 + h * 16;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const float4 v = cp[q];
+        d[2 * q] = cheb(zi, make_float2(v.x, v.y));
+        d[2 * q + 1] = cheb(zi, make_float2(v.z, v.w));
       }
-      if (!need) {
-        if (dir) hhi = nch; else hlo = -1;
-        continue;
+      if (MULTI) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          below += d[q] <= floor_ ? 1 : 0;
+          d[q] = d[q] <= floor_ ? INFINITY : d[q];
+        }
       }
-      exact = dir ? (hc == c1) : (hc == c0 - 1);
-      h = hc;
-      if (dir) ++hhi; else --hlo;
-      found = true;
+      bool merge = exact;
+      if (!merge) {
+        float m = d[0];
+#pragma unroll
+        for (int q = 1; q < 32; ++q) m = fminf(m, d[q]);
+        merge = __any_sync(0xffffffffu, m < l[KT]);
+      }
+      if (merge) batch_merge32(l, d);
+      if (h != c0) ncand += min(32, n - h * 32);
+      // next chunk: alternate directions; a direction ends at the array edge or by the sweep test
+      bool found = false;
+#pragma unroll 1
+      for (int tries = 0; tries < 2 && !found; ++tries) {
+        dir ^= 1;
+        const int hc = dir ? hhi : hlo;
+        if (dir ? hc >= nch : hc < 0) continue;
+        bool need = true;
+        if (SWEEP) {
+          const float xe = xy[hc * 32 + (dir ? 0 : 31)].x;
+          const float gap = dir ? xe - zi.x : zi.x - xe;
+          need = __any_sync(0xffffffffu, (ti < n) && (gap < l[KT]));
+        }
+        if (!need) {
+          if (dir) hhi = nch; else hlo = -1;
+          continue;
+        }
+        exact = dir ? (hc == c1) : (hc == c0 - 1);
+        h = hc;
+        if (dir) ++hhi; else --hlo;
+        found = true;
+      }
+      if (!found) break;
     }
-    if (!found) break;
+    // (k+1)-th smallest including the member itself (R3): rank k - below within this pass's list
+    // r < 0: more than k values lie at or below the floor, i.e. rank k falls on the tie copies of
+    // the floor value that the previous pass could not list -> eps = floor
+    const int r = k - below;
+    if (!done && r < 32) {
+      float v = r < 0 ? floor_ : l[0];
+#pragma unroll
+      for (int t = 1; t < 32; ++t)
+        if (t == r) v = l[t];
+      e = v;
+      done = true;
+    }
+    if (!MULTI || __all_sync(0xffffffffu, done)) break;
+    floor_ = done ? INFINITY : l[31];  // finished lanes: every candidate is "below", no merges
   }
   const int valid = min(32, n - mb * 32);
   int nb = 0;
@@ -532,10 +569,6 @@ __device__ __forceinline__ int ksg_block_big(const float2* __restrict__ xy, cons
     if (next_blk) nb = atomicAdd(next_blk, 1);
   }
   if (ti < n) {
-    float e = l[0];
-#pragma unroll
-    for (int t = 1; t < 32; ++t)
-      if (t == k) e = l[t];  // (k+1)-th smallest including the member itself
     int cu, cv;
     marginal_counts(xy, sy, log2p, zi.x, zi.y, e, cu, cv);
     acc += __ldg(psi + cu + off) + __ldg(psi + cv + off);
@@ -646,11 +679,12 @@ __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? (
     double acc = 0.0;
     // member blocks: first one static, then dynamic (sweep lengths differ per block)
     for (int mb = warp; mb < nblk;) {
-      if constexpr (RM == 1 && (K == 30 || K == 31)) {
+      if constexpr (RM == 1 && (K == 30 || K == 31 || K == 64)) {
         // batched 32-entry lists including the member itself: K is the threshold index l[K]
         // (K = 30 for the paper's k = 30; K = 31 serves 24 < k <= 31)
-        mb = ksg_block_big<K, SWEEP>(xy, sy, n, nch, log2p, mb, lane, k, psi, off, acc, executed,
-                                                      out, u, pm, swap, next_blk);
+        // K = 64 marks the multi-pass lists for k >= 33 (threshold index l[31])
+        mb = ksg_block_big<(K < 32 ? K : 31), SWEEP, (K == 64)>(xy, sy, n, nch, log2p, mb, lane, k, psi, off, acc,
+                                                                 executed, out, u, pm, swap, next_blk);
       } else {
         mb = ksg_block<K, RM, G, SWEEP, false>(xy, sy, dupbuf + warp * 64, n, nch, log2p, mb, lane, k, psi, off,
                                                acc, executed, out, u, pm, swap, next_blk);
@@ -906,7 +940,9 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool p
                             : launch_t<31, 1, 4, false>(fa, fb, k, plus1, src, out, st);
   if (k <= 32) return sweep ? launch_t<32, 1, 4, true>(fa, fb, k, plus1, src, out, st)
                             : launch_t<32, 1, 4, false>(fa, fb, k, plus1, src, out, st);
-  return cudaErrorNotSupported;
+  // k >= 33 (up to n - 1): multi-pass 32-entry batched lists (ksg_block_big<31, SWEEP, true>)
+  return sweep ? launch_t<64, 1, 4, true>(fa, fb, k, plus1, src, out, st)
+               : launch_t<64, 1, 4, false>(fa, fb, k, plus1, src, out, st);
 }
 
 cudaError_t ksg_cell_comparisons(unsigned long long* value, bool reset);

@@ -504,3 +504,40 @@ def test_batch_equals_single_calls(n):
                                  for i in range(len(a))])
         assert np.array_equal(batch, single, equal_nan=True), measure
     f.close()
+
+
+@pytest.mark.parametrize("n,k,npairs", [(2000, 0, 10), (4096, 0, 3), (1000, 33, 12), (1000, 64, 10),
+                                        (100, 50, 40), (100, 99, 40), (300, 200, 8), (130, 97, 16)])
+def test_large_k_multipass(n, k, npairs):
+    """k >= 33 (the paper's k = ceil(3n/100) for n >= 1067: 60 at n = 2000, 123 at n = 4096;
+    PAPER.md:173) runs the multi-pass batched lists: eps / counts bit-exact vs the oracle, MI
+    within 1e-4, and the pruned and dense passes bit-identical (incl. k = n - 1)."""
+    spec = synth.field_spec(4, 4, 2, n, seed=3 * n + k)
+    vals, f = _field(spec)
+    a, b = synth.random_pairs(spec.points, npairs, seed=n + k)
+    a, b = a.numpy(), b.numpy()
+    kk = k if k else min(max(1, -(-3 * n // 100)), n - 1)
+    assert kk >= 33
+    _check_knn(f, vals, kk, a, b)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    got = _cpu(cb.corr_eval_pairs(f, None, cb.CORR_KSG, k, ta, tb))
+    dense = _cpu(cb.corr_eval_pairs(f, None, cb.CORR_KSG | cb.CORR_F_KSG_DENSE, k, ta, tb))
+    ref = oracle.eval_pairs(vals.cpu(), None, oracle.KSG, kk, a, b)
+    assert np.array_equal(got, dense, equal_nan=True)
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    ok = ~np.isnan(ref)
+    assert np.max(np.abs(got[ok] - ref[ok]), initial=0) <= KSG_TOL
+    f.close()
+
+
+@pytest.mark.parametrize("k", [33, 64, 100])
+def test_large_k_multipass_ties(k):
+    """Heavily quantised series (many equal distances at every pass's floor): the multi-pass
+    lists must count the floor's tie copies exactly (eps may equal the floor value)."""
+    n, P = 200, 64
+    g = torch.Generator().manual_seed(k)
+    vals = (torch.randint(0, 6, (n, P), generator=g).to(torch.float32) * 0.5).contiguous()
+    f = cb.corr_field_create(vals.cuda(), 8, 8, 1, n)
+    a, b = synth.random_pairs(P, 60, seed=k)
+    _check_knn(f, vals, k, a.numpy(), b.numpy())
+    f.close()
