@@ -247,16 +247,24 @@ int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset) {
 
 namespace corr {
 namespace {
+// Resident device copies of small host tables (region / tile lists), keyed by content (the lists
+// are seed-free, so a context view's table is uploaded once).  No host synchronisation: the upload
+// is stream-ordered on the first caller's stream and an event marks it ready; every user's stream
+// waits on that event and records a last-use event.  Least-recently-used entries are evicted
+// (freed stream-ordered after their last use) when the byte budget would be exceeded.
 struct TableEntry {
   int device;
   uint64_t hash;
   std::vector<unsigned char> bytes;
   void* dptr;
+  cudaEvent_t ready, last_use;
+  uint64_t tick;
 };
 std::mutex g_table_mu;
 std::vector<TableEntry> g_tables;
 size_t g_table_bytes = 0;
-constexpr size_t kTableCacheBytes = 256u << 20;
+uint64_t g_table_tick = 0;
+constexpr size_t kTableCacheBytes = 64u << 20;
 uint64_t fnv1a(const unsigned char* p, size_t n) {
   uint64_t h = 1469598103934665603ull;
   for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
@@ -268,24 +276,45 @@ const void* cached_table(int device, const void* host, size_t bytes, cudaStream_
   const unsigned char* hp = static_cast<const unsigned char*>(host);
   const uint64_t h = fnv1a(hp, bytes);
   std::lock_guard<std::mutex> lock(g_table_mu);
-  for (const TableEntry& t : g_tables)
-    if (t.device == device && t.hash == h && t.bytes.size() == bytes && memcmp(t.bytes.data(), hp, bytes) == 0)
+  for (TableEntry& t : g_tables)
+    if (t.device == device && t.hash == h && t.bytes.size() == bytes && memcmp(t.bytes.data(), hp, bytes) == 0) {
+      if (cudaStreamWaitEvent(st, t.ready, 0) != cudaSuccess || cudaEventRecord(t.last_use, st) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      t.tick = ++g_table_tick;
       return t.dptr;
-  if (g_table_bytes + bytes > kTableCacheBytes) return nullptr;  // caller falls back to a per-call copy
-  void* d = nullptr;
-  if (cudaMalloc(&d, bytes) != cudaSuccess) {
+    }
+  if (bytes > kTableCacheBytes) return nullptr;  // caller falls back to a per-call copy
+  while (g_table_bytes + bytes > kTableCacheBytes) {  // evict this device's least recently used entry
+    long lru = -1;
+    for (size_t i = 0; i < g_tables.size(); ++i)
+      if (g_tables[i].device == device && (lru < 0 || g_tables[i].tick < g_tables[(size_t)lru].tick)) lru = (long)i;
+    if (lru < 0) return nullptr;  // the budget is held by other devices' tables: per-call copy
+    TableEntry& t = g_tables[(size_t)lru];
+    cudaStreamWaitEvent(st, t.last_use, 0);  // freed on this stream after its last use
+    cudaFreeAsync(t.dptr, st);
+    cudaEventDestroy(t.ready);
+    cudaEventDestroy(t.last_use);
+    g_table_bytes -= t.bytes.size();
+    g_tables.erase(g_tables.begin() + lru);
+  }
+  TableEntry t{device, h, std::vector<unsigned char>(hp, hp + bytes), nullptr, nullptr, nullptr, ++g_table_tick};
+  // stream-ordered upload; pageable host memory is consumed before cudaMemcpyAsync returns
+  if (cudaMallocAsync(&t.dptr, bytes, st) != cudaSuccess ||
+      cudaMemcpyAsync(t.dptr, host, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&t.last_use, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(t.ready, st) != cudaSuccess || cudaEventRecord(t.last_use, st) != cudaSuccess) {
     cudaGetLastError();
+    if (t.dptr) cudaFreeAsync(t.dptr, st);
+    if (t.ready) cudaEventDestroy(t.ready);
+    if (t.last_use) cudaEventDestroy(t.last_use);
     return nullptr;
   }
-  // first use: ordered on the caller's stream (tables are immutable afterwards)
-  if (cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-      cudaStreamSynchronize(st) != cudaSuccess) {
-    cudaFree(d);
-    return nullptr;
-  }
-  g_tables.push_back(TableEntry{device, h, std::vector<unsigned char>(hp, hp + bytes), d});
   g_table_bytes += bytes;
-  return d;
+  g_tables.push_back(std::move(t));
+  return g_tables.back().dptr;
 }
 }  // namespace corr
 
@@ -479,7 +508,6 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
     R.B = regionB[r];
     R.nA = (int64_t)(R.A.x1 - R.A.x0) * (R.A.y1 - R.A.y0) * (R.A.z1 - R.A.z0);
     R.nB = (int64_t)(R.B.x1 - R.B.x0) * (R.B.y1 - R.B.y0) * (R.B.z1 - R.B.z0);
-    R.key = region_key(seed, R.A, R.B);
     R.off = total;
     if (samples == 0 && R.nA * R.nB >= ((int64_t)1 << 32))
       return fail(CORR_E_INVAL, "exhaustive region pair with |A|*|B| >= 2^32");
@@ -496,15 +524,19 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
   const bool own_reg = dreg == nullptr;
   cudaError_t e = cudaSuccess;
   if (own_reg) e = cudaMallocAsync((void**)&dreg, reg_bytes, st);
+  uint64_t* rkey = nullptr;  // sampler keys of this call's seed, derived on the device
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&keys, (size_t)nregion_pairs * 8, st);
+  if (e == cudaSuccess && samples > 0) e = cudaMallocAsync((void**)&rkey, (size_t)nregion_pairs * 8, st);
   if (e != cudaSuccess) return cuda_fail(e, "corr_region_max alloc");
   if (own_reg) e = cudaMemcpyAsync(dreg, reg.data(), reg_bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(keys, 0, (size_t)nregion_pairs * 8, st);
+  if (e == cudaSuccess && rkey) e = launch_region_keys(dreg, nregion_pairs, seed, rkey, st);
 
   PairSrc src;
   memset(&src, 0, sizeof(src));
   src.mode = samples > 0 ? kSampled : kExhaustive;
   src.reg = dreg;
+  src.rkey = rkey;
   src.nreg = nregion_pairs;
   src.samples = samples;
   src.nunits = total;
@@ -523,6 +555,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
       if (e == cudaErrorNotSupported) {
         if (own_reg) cudaFreeAsync(dreg, st);
         cudaFreeAsync(keys, st);
+        if (rkey) cudaFreeAsync(rkey, st);
         return fail(CORR_E_INVAL, "KSG configuration not supported");
       }
     } else if (samples == 0) {
@@ -538,6 +571,7 @@ int corr_region_max(const corr_field* fa, const corr_field* fb, int32_t measure,
   if (e == cudaSuccess) e = launch_region_finalize(src, keys, out_max, out_argmax, st);
   if (own_reg) cudaFreeAsync(dreg, st);
   cudaFreeAsync(keys, st);
+  if (rkey) cudaFreeAsync(rkey, st);
   if (e != cudaSuccess) return cuda_fail(e, "corr_region_max");
   return CORR_OK;
 }

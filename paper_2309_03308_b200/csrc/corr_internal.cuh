@@ -41,10 +41,11 @@ constexpr int kSMs = 148;
 extern std::atomic<long long> g_launch_count;  // kernels launched (corr_launch_count)
 inline void note_launch(int k = 1) { g_launch_count.fetch_add(k, std::memory_order_relaxed); }
 
-// A region pair on the device (boxes, sampler key, sizes, exhaustive offsets).
+// A region pair on the device (boxes, sizes, exhaustive offsets).  Seed-free, so the resident
+// table (cached_table) is reused by calls with any seed; the seed-dependent sampler keys live in
+// a per-call device array (PairSrc::rkey, filled by launch_region_keys).
 struct RegionDev {
   corr_box A, B;
-  uint64_t key;  // sampler key h_12 (reading R15)
   int64_t nA, nB;
   int64_t off;   // exhaustive mode: prefix sum of nA*nB
 };
@@ -56,6 +57,7 @@ struct PairSrc {
   const int64_t* idxA;
   const int64_t* idxB;
   const RegionDev* reg;
+  const uint64_t* rkey;  // kSampled: sampler key h_12 per region pair (reading R15)
   int64_t nreg;
   int64_t samples;
   int64_t nunits;
@@ -100,6 +102,8 @@ const void* cached_table(int device, const void* host, size_t bytes, cudaStream_
 cudaError_t gemm_flops(unsigned long long* value /* [2]: bf16, tf32 */, bool reset);
 cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
                                  const PairOut& out, cudaStream_t st);
+// rkey[r] = the sampler key of region pair r for `seed` (R15), computed on the device.
+cudaError_t launch_region_keys(const RegionDev* dreg, int64_t nreg, uint64_t seed, uint64_t* rkey, cudaStream_t st);
 cudaError_t launch_region_finalize(const PairSrc& src, const unsigned long long* keys,
                                    float* out_max, int64_t* out_argmax, cudaStream_t st);
 // tcgen05 split-TF32 block GEMM with fused max/argmax epilogue (pearson_gemm.cu).

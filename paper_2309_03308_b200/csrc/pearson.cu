@@ -173,6 +173,12 @@ __global__ void __launch_bounds__(256) pearson_exact_selected_kernel(const float
   }
 }
 
+__global__ void region_keys_kernel(const RegionDev* __restrict__ reg, int64_t nreg, uint64_t seed,
+                                   uint64_t* __restrict__ rkey) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nreg) rkey[r] = region_key(seed, reg[r].A, reg[r].B);
+}
+
 __global__ void region_finalize_kernel(PairSrc src, const unsigned long long* __restrict__ keys,
                                        float* __restrict__ out_max, int64_t* __restrict__ out_arg) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -188,7 +194,7 @@ __global__ void region_finalize_kernel(PairSrc src, const unsigned long long* __
   const RegionDev& R = src.reg[r];
   int64_t a, b;
   if (src.mode == kSampled) {
-    const uint64_t v = mix64(R.key + kGolden * (uint64_t)((int64_t)idx + 1));
+    const uint64_t v = mix64(src.rkey[r] + kGolden * (uint64_t)((int64_t)idx + 1));
     a = box_to_point(R.A, (int64_t)(((v & 0xFFFFFFFFULL) * (uint64_t)R.nA) >> 32), src.nx, src.ny);
     b = box_to_point(R.B, (int64_t)(((v >> 32) * (uint64_t)R.nB) >> 32), src.nx, src.ny);
   } else {
@@ -202,6 +208,13 @@ __global__ void region_finalize_kernel(PairSrc src, const unsigned long long* __
 }
 
 }  // namespace
+
+cudaError_t launch_region_keys(const RegionDev* dreg, int64_t nreg, uint64_t seed, uint64_t* rkey, cudaStream_t st) {
+  if (nreg == 0) return cudaSuccess;
+  region_keys_kernel<<<(unsigned)((nreg + 255) / 256), 256, 0, st>>>(dreg, nreg, seed, rkey);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, const PairSrc& src,
                                  const PairOut& out, cudaStream_t st) {

@@ -22,7 +22,7 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-inline uint64_t region_key(uint64_t seed, const corr_box& A, const corr_box& B) {
+__host__ __device__ inline uint64_t region_key(uint64_t seed, const corr_box& A, const corr_box& B) {
   const int32_t c[12] = {A.x0, A.y0, A.z0, A.x1, A.y1, A.z1, B.x0, B.y0, B.z0, B.x1, B.y1, B.z1};
   uint64_t h = seed;
   for (int t = 0; t < 12; ++t) h = mix64(h ^ ((uint64_t)(uint32_t)c[t] + kGolden * (uint64_t)(t + 1)));
@@ -68,7 +68,7 @@ __device__ __forceinline__ bool unit_pair(const PairSrc& s, int64_t u, int64_t& 
     r = u / s.samples;
     const int64_t smp = u - r * s.samples;
     const RegionDev& R = s.reg[r];
-    const uint64_t v = mix64(R.key + kGolden * (uint64_t)(smp + 1));
+    const uint64_t v = mix64(s.rkey[r] + kGolden * (uint64_t)(smp + 1));
     const uint64_t al = ((v & 0xFFFFFFFFULL) * (uint64_t)R.nA) >> 32;
     const uint64_t bl = ((v >> 32) * (uint64_t)R.nB) >> 32;
     a = box_to_point(R.A, (int64_t)al, s.nx, s.ny);
