@@ -165,6 +165,13 @@ int corr_check(const corr_field* f, void* cuda_stream);
  * the counter after reading.  Diagnostic for the roofline report (bench.py). */
 int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset);
 
+/* corr_ksg_nan_pairs -- KSG point pairs that corr_region_max skipped on `device` since the last
+ * reset because their value was NaN: a constant series (reading R10), or psi(0) in the verbatim
+ * form when a member's joint sample is duplicated (eps = 0, reading R5; e.g. zero-inflated
+ * fields).  Such pairs never win a region maximum; this count makes their number visible.
+ * Synchronises the device; reset != 0 zeroes the counter after reading. */
+int corr_ksg_nan_pairs(int32_t device, int64_t* count, int32_t reset);
+
 /* corr_gemm_flops -- tensor-core work executed on `device` by the exhaustive Pearson block path
  * (corr_region_max with samples == 0) since the last reset, as logical MMA flops 2*128*256*K per
  * 128x256 tile and MMA set: *bf16_flops for the screening pass (one bf16 product per tile),

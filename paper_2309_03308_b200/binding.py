@@ -25,7 +25,7 @@ CORR_F_KSG_COUNT = 1 << 11
 CORR_OK, CORR_E_INVAL, CORR_E_RANGE, CORR_E_NOMEM, CORR_E_CUDA = 0, -1, -2, -3, -4
 
 EXPORTS = ("corr_field_create", "corr_field_update", "corr_field_aggregate", "corr_field_destroy", "corr_field_info", "corr_eval_pairs",
-           "corr_region_max", "corr_ksg_debug", "corr_check", "corr_ksg_comparisons", "corr_gemm_flops", "corr_launch_count",
+           "corr_region_max", "corr_ksg_debug", "corr_check", "corr_ksg_comparisons", "corr_ksg_nan_pairs", "corr_gemm_flops", "corr_launch_count",
            "corr_last_error")
 
 
@@ -67,6 +67,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     L.corr_check.argtypes = [vp, vp]
     L.corr_launch_count.argtypes = []
     L.corr_ksg_comparisons.argtypes = [i32, ctypes.POINTER(i64), i32]
+    L.corr_ksg_nan_pairs.argtypes = [i32, ctypes.POINTER(i64), i32]
     L.corr_gemm_flops.argtypes = [i32, ctypes.POINTER(i64), ctypes.POINTER(i64), i32]
     L.corr_last_error.restype = ctypes.c_char_p
     L.corr_last_error.argtypes = []
@@ -232,6 +233,13 @@ def corr_ksg_debug(fa: Field, fb: Optional[Field], k: int, idxA: torch.Tensor, i
 def corr_ksg_comparisons(device: int = 0, reset: bool = True) -> int:
     v = ctypes.c_int64()
     _check(load().corr_ksg_comparisons(device, ctypes.byref(v), int(reset)))
+    return v.value
+
+
+def corr_ksg_nan_pairs(device: int = 0, reset: bool = True) -> int:
+    """KSG point pairs corr_region_max skipped as NaN (constant series, psi(0)) since the last reset."""
+    v = ctypes.c_int64()
+    _check(load().corr_ksg_nan_pairs(device, ctypes.byref(v), int(reset)))
     return v.value
 
 

@@ -243,6 +243,18 @@ int corr_ksg_comparisons(int32_t device, int64_t* count, int32_t reset) {
   return CORR_OK;
 }
 
+int corr_ksg_nan_pairs(int32_t device, int64_t* count, int32_t reset) {
+  if (!count) return fail(CORR_E_INVAL, "count is NULL");
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long v = 0;
+  if (e == cudaSuccess) e = ksg_nan_pairs(&v, reset != 0);
+  if (e != cudaSuccess) return cuda_fail(e, "corr_ksg_nan_pairs");
+  *count = (int64_t)v;
+  return CORR_OK;
+}
+
 }  // extern "C"
 
 namespace corr {

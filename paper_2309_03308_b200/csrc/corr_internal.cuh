@@ -94,6 +94,7 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool p
 cudaError_t launch_ksg_cell(const corr_field* fa, const corr_field* fb, int k, bool plus1, bool count,
                             const PairSrc& src, const PairOut& out, cudaStream_t st);
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset);
+cudaError_t ksg_nan_pairs(unsigned long long* value, bool reset);
 // Device copy of a small host table (region lists) that stays resident and is reused when the
 // same bytes come again: no host->device copy on the call path of repeated calls.  (A small copy
 // queued behind a large pinned upload on the same copy engine would otherwise stall the stream

@@ -35,6 +35,7 @@
 namespace corr {
 
 __device__ unsigned long long g_ksg_comparisons;  // executed comparisons (corr_ksg_comparisons)
+__device__ unsigned long long g_ksg_nan_pairs;    // region-max pairs skipped as NaN (corr_ksg_nan_pairs)
 
 namespace {
 
@@ -621,7 +622,7 @@ __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? (
   const uint32_t row_bytes = (uint32_t)n_pad * 4u;
   const double psi_nk = __ldg(psi + n) + __ldg(psi + k);
   const int off = plus1 ? 1 : 0;
-  unsigned long long executed = 0;
+  unsigned long long executed = 0, nan_pairs = 0;
 
   for (int64_t u = blockIdx.x; u < src.nunits; u += gridDim.x) {
     int64_t a, b, r;
@@ -634,6 +635,7 @@ __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? (
     const bool degenerate = (ca[a] | cb[b]) != 0;
     if (degenerate && out.dbg_eps == nullptr) {
       if (src.mode == kList && threadIdx.x == 0) out.out[u] = NAN;
+      else if (threadIdx.x == 0) ++nan_pairs;
       continue;
     }
     // sort along the wider marginal (swap roles of x and y; exact by Eq. 1 symmetry)
@@ -702,10 +704,13 @@ __global__ void __launch_bounds__(RM == 1 ? 128 : 256, (K > 8 ? 4 : (RM == 1 ? (
         out.out[u] = mi;
       } else if (!isnan(mi)) {
         atomicMax(out.keys + r, pack_key(out.absval ? fabsf(mi) : mi, idx));
+      } else {
+        ++nan_pairs;
       }
     }
   }
   if (lane == 0 && executed) atomicAdd(&g_ksg_comparisons, executed);
+  if (threadIdx.x == 0 && nan_pairs) atomicAdd(&g_ksg_nan_pairs, nan_pairs);
 }
 
 template <int K, int RM, int G, bool SWEEP>
@@ -792,7 +797,7 @@ __global__ void __launch_bounds__(128, 8) ksg_warp_kernel(
   const uint32_t row_bytes = (uint32_t)n_pad * 4u;
   const double psi_nk = __ldg(psi + n) + __ldg(psi + k);
   const int off = plus1 ? 1 : 0;
-  unsigned long long executed = 0;
+  unsigned long long executed = 0, nan_pairs = 0;
   const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t u0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
 
@@ -832,6 +837,7 @@ __global__ void __launch_bounds__(128, 8) ksg_warp_kernel(
     const WarpSlotMeta m = meta[s];
     if (!(m.flags & 1) || !(m.flags & 8)) {  // invalid / self pair, or degenerate without debug dump
       if (src.mode == kList && lane == 0) out.out[u] = NAN;
+      else if (lane == 0 && (m.flags & 1)) ++nan_pairs;  // a constant series: NaN, skipped
       __syncwarp();
       continue;
     }
@@ -857,11 +863,14 @@ __global__ void __launch_bounds__(128, 8) ksg_warp_kernel(
         out.out[u] = mi;
       } else if (!isnan(mi)) {
         atomicMax(out.keys + m.r, pack_key(out.absval ? fabsf(mi) : mi, m.idx));
+      } else {
+        ++nan_pairs;
       }
     }
     __syncwarp();  // slot s and xy are free: the next iteration's issue may overwrite slot s
   }
   if (lane == 0 && executed) atomicAdd(&g_ksg_comparisons, executed);
+  if (lane == 0 && nan_pairs) atomicAdd(&g_ksg_nan_pairs, nan_pairs);
 }
 
 template <int K, bool SWEEP>
@@ -946,6 +955,19 @@ cudaError_t launch_ksg(const corr_field* fa, const corr_field* fb, int k, bool p
 }
 
 cudaError_t ksg_cell_comparisons(unsigned long long* value, bool reset);
+cudaError_t ksg_cell_nan_pairs(unsigned long long* value, bool reset);
+
+cudaError_t ksg_nan_pairs(unsigned long long* value, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(value, g_ksg_nan_pairs, sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long zero = 0;
+    e = cudaMemcpyToSymbol(g_ksg_nan_pairs, &zero, sizeof(zero));
+  }
+  unsigned long long cell = 0;
+  if (e == cudaSuccess) e = ksg_cell_nan_pairs(&cell, reset);
+  *value += cell;
+  return e;
+}
 
 cudaError_t ksg_comparisons(unsigned long long* value, bool reset) {
   cudaError_t e = cudaMemcpyFromSymbol(value, g_ksg_comparisons, sizeof(unsigned long long));

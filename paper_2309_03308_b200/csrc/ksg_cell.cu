@@ -34,6 +34,7 @@ namespace corr {
 // executed comparisons of this kernel (no relocatable device code: ksg.cu's counter is not
 // visible here; ksg_comparisons() reads both)
 __device__ unsigned long long g_ksg_cell_comparisons;
+__device__ unsigned long long g_ksg_cell_nan_pairs;  // region-max pairs skipped as NaN
 
 namespace {
 
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 8 : 4)) ksg_cell_kernel(
   const uint32_t row_bytes = (uint32_t)n_pad * 4u;
   const double psi_nk = __ldg(psi + n) + __ldg(psi + k);
   const int off = plus1 ? 1 : 0;
-  unsigned long long executed = 0;
+  unsigned long long executed = 0, nan_pairs = 0;
 
   for (int64_t u = blockIdx.x; u < src.nunits; u += gridDim.x) {
     int64_t a, b, r;
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 8 : 4)) ksg_cell_kernel(
     const bool degenerate = (ca[a] | cb[b]) != 0;
     if (degenerate && out.dbg_eps == nullptr) {
       if (src.mode == kList && tid == 0) out.out[u] = NAN;
+      else if (tid == 0) ++nan_pairs;
       continue;
     }
     const bool swap = spb[b] > spa[a];  // x = the wider marginal
@@ -347,10 +349,13 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 8 : 4)) ksg_cell_kernel(
         out.out[u] = mi;
       } else if (!isnan(mi)) {
         atomicMax(out.keys + r, pack_key(out.absval ? fabsf(mi) : mi, idx));
+      } else {
+        ++nan_pairs;
       }
     }
   }
   if (lane == 0 && executed) atomicAdd(&g_ksg_cell_comparisons, executed);
+  if (tid == 0 && nan_pairs) atomicAdd(&g_ksg_cell_nan_pairs, nan_pairs);
 }
 
 template <int K, int NW>
@@ -379,6 +384,15 @@ cudaError_t ksg_cell_comparisons(unsigned long long* value, bool reset) {
   if (e == cudaSuccess && reset) {
     const unsigned long long zero = 0;
     e = cudaMemcpyToSymbol(g_ksg_cell_comparisons, &zero, sizeof(zero));
+  }
+  return e;
+}
+
+cudaError_t ksg_cell_nan_pairs(unsigned long long* value, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(value, g_ksg_cell_nan_pairs, sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long zero = 0;
+    e = cudaMemcpyToSymbol(g_ksg_cell_nan_pairs, &zero, sizeof(zero));
   }
   return e;
 }

@@ -344,6 +344,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i)
             if (cpt[ch * 32 + i] == pa) v[i] = -INFINITY;
         }
+        if (!SCREEN) {
+          // clamp to [-1, 1] BEFORE the max / first-index search (masked entries stay -inf), so
+          // split-TF32 values rounding above 1 tie at 1 and the lowest q wins (R16), as in the
+          // sampled path
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = v[i] > -INFINITY ? fminf(1.f, fmaxf(-1.f, v[i])) : v[i];
+        }
         float m = v[0];
 #pragma unroll
         for (int i = 1; i < 32; ++i) m = fmaxf(m, v[i]);
@@ -670,6 +677,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i)
             if (cpt[ch * 32 + i] == pa) v[i] = -INFINITY;
         }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = v[i] > -INFINITY ? fminf(1.f, fmaxf(-1.f, v[i])) : v[i];  // as above
         float m = v[0];
 #pragma unroll
         for (int i = 1; i < 32; ++i) m = fmaxf(m, v[i]);

@@ -541,3 +541,29 @@ def test_large_k_multipass_ties(k):
     a, b = synth.random_pairs(P, 60, seed=k)
     _check_knn(f, vals, k, a.numpy(), b.numpy())
     f.close()
+
+
+@pytest.mark.parametrize("n", [100, 300])
+def test_ksg_nan_pairs_counted(n):
+    """Zero-inflated series (R5: duplicate joint samples -> eps = 0 -> psi(0) -> NaN) and constant
+    series (R10): corr_region_max skips their NaN values, and corr_ksg_nan_pairs reports exactly
+    the number of skipped sampled pairs the oracle's enumeration finds NaN (warp kernel at n = 100,
+    column-cell kernel at n = 300)."""
+    nx, ny, nz = 8, 8, 2
+    g = torch.Generator().manual_seed(n)
+    vals = torch.rand((n, nx * ny * nz), generator=g)
+    vals[torch.rand(vals.shape, generator=g) < 0.4] = 0.0
+    vals[:, 5] = 1.5  # a constant series
+    vals = vals.contiguous()
+    f = cb.corr_field_create(vals.cuda(), nx, ny, nz, n)
+    boxes = synth.partition(nx, ny, nz, 4, 4, 2)
+    A, B = synth.context_pairs(boxes)
+    S = 64
+    cb.corr_ksg_nan_pairs(0, reset=True)
+    gm, ga = cb.corr_region_max(f, None, cb.CORR_KSG, 3, A, B, S, 5)
+    got = cb.corr_ksg_nan_pairs(0, reset=True)
+    vals_o, va, vb = oracle.region_values(vals, None, (nx, ny, nz), oracle.KSG, 3, A, B, S, 5)
+    assert got == int(np.isnan(vals_o).sum()) and got > 0
+    mx, arg, sec, value_at = oracle_region_reference(vals, None, (nx, ny, nz), oracle.KSG, 3, A, B, S, 5)
+    assert_region_argmax(_cpu(gm), _cpu(ga), mx, arg, sec, KSG_TOL, value_at)
+    f.close()
