@@ -390,7 +390,7 @@ def main():
     fa_box, fb_box = slabs[rank], fB
     nA = (fa_box[3] - fa_box[0]) * (fa_box[4] - fa_box[1]) * (fa_box[5] - fa_box[2])
     nB = (fb_box[3] - fb_box[0]) * (fb_box[4] - fb_box[1]) * (fb_box[5] - fb_box[2])
-    tf32_peak = (peaks.get("bf16_tflops") or 1664.4) * 0.5
+    tf32_peak = (peaks.get("bf16_tflops") or 1612.0) * 0.5
     tf32_ctx = None  # cuBLAS TF32 GEMM measured on this pool (profiles/r01_tf32_peak.json), context only
     try:
         tf32_ctx = json.load(open(os.path.join(ROOT, "profiles", "r01_tf32_peak.json")))["tf32_tflops_burst"]
@@ -400,7 +400,7 @@ def main():
     # exact pass over the tiles that can hold the maximum; dense-equivalent work reported beside it
     # mixed precision: the peak is the flop-weighted harmonic blend of the bf16 and tf32 peaks, so
     # frac = (bf16 flops / bf16 peak + tf32 flops / tf32 peak) / time
-    bf16_peak = peaks.get("bf16_tflops") or 1664.4
+    bf16_peak = peaks.get("bf16_tflops") or 1612.0
     blk_s = stage_ms["pearson_block"] / 1e3
     blk_tflops = (gemm_bf16 + gemm_tf32) / blk_s / 1e12
     at_peak_s = (gemm_bf16 / bf16_peak + gemm_tf32 / tf32_peak) / 1e12

@@ -2,6 +2,8 @@
 // Measures warp-instructions issued per SM per cycle (clock64 per block) for
 // FMNMX, FMNMX3, FADD, FADD2, FFMA, IADD3, packed f16/bf16/s16 min-max, HADD2, HSETP2, F2FP, LOP3
 // and mixes. Informs DESIGN.md's ALU roofline.
+// Build (the binary is not tracked): nvcc -gencode arch=compute_100a,code=sm_100a -O3 \
+//   -o tools/pipe_microbench tools/pipe_microbench.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
