@@ -13,6 +13,7 @@
 //   cflag          constant series (min == max) -> NaN correlations (reading R10)
 // All kernels are HBM-bound; DESIGN.md lists their algorithmic bytes.
 #include <math.h>
+#include <stdlib.h>
 
 #include <cuda_bf16.h>
 
@@ -232,6 +233,182 @@ __global__ void __launch_bounds__(T) sort_radix_kernel(const float* __restrict__
   }
 }
 
+// ---- 3c. per-row bucket sort (one CTA of 128 threads per row, persistent over rows) ----------
+// The radix sort above needs ~5 ranked passes per row; ensemble rows are smooth distributions,
+// so one pass of BUCKETING plus tiny per-bucket sorts does the same job: keys u (order-preserving
+// u32, as above) map to NB buckets by b = floor((u - kmin) * NB / (kmax - kmin + 1)) computed in
+// fp32 -- a monotone non-decreasing map (monotone rounding), so bucket order is key order -- with
+// a shared-memory histogram whose atomic return value is the slot inside the bucket; after an
+// exclusive scan the row is scattered by bucket and every key's final position is its bucket
+// start plus its rank inside the bucket (about n/NB <= 0.5 keys per bucket).  Equal keys may land in any order: consumers only need SOME sorted
+// permutation (R4).  Rows whose largest bucket exceeds kMaxBucket (heavy outliers stretching the
+// range) are sorted by a block bitonic network instead, so no row costs O(n^2).
+constexpr int kBucketThreads = 128;
+constexpr int kMaxBucket = 48;
+
+__device__ __forceinline__ uint32_t ord_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return u ^ ((u >> 31) ? 0xFFFFFFFFu : 0x80000000u);
+}
+__device__ __forceinline__ float key_float(uint32_t u) {
+  return __uint_as_float(u ^ ((u >> 31) ? 0x80000000u : 0xFFFFFFFFu));
+}
+
+template <int NB, int N2>
+__global__ void __launch_bounds__(kBucketThreads) sort_bucket_kernel(const float* __restrict__ F, float* __restrict__ S,
+                                                                     uint16_t* __restrict__ perm, int n, int n_pad,
+                                                                     int64_t P) {
+  __shared__ uint32_t key[N2];     // bucketed keys (then, on the fallback, the bitonic array)
+  __shared__ uint16_t idx[N2];
+  __shared__ uint32_t raw[N2];     // the row's keys in member order
+  __shared__ uint32_t sk[N2];      // sorted keys / member indices (bucket path)
+  __shared__ uint16_t si[N2];
+  __shared__ int cnt[NB + 1];
+  __shared__ uint32_t red[4][2];
+  __shared__ int maxb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
+    const float* row = F + p * n_pad;
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+    for (int e = tid; e < n; e += kBucketThreads) {
+      const uint32_t u = ord_key(row[e]);
+      raw[e] = u;
+      kmin = min(kmin, u);
+      kmax = max(kmax, u);
+    }
+    for (int b = tid; b <= NB; b += kBucketThreads) cnt[b] = 0;
+    if (tid == 0) maxb = 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) {
+      red[warp][0] = kmin;
+      red[warp][1] = kmax;
+    }
+    __syncthreads();
+    kmin = min(min(red[0][0], red[1][0]), min(red[2][0], red[3][0]));
+    kmax = max(max(red[0][1], red[1][1]), max(red[2][1], red[3][1]));
+    const float scale = (float)NB / ((float)(kmax - kmin) + 1.0f);
+    // histogram: the atomic's return value is the key's slot inside its bucket
+    int slot[N2 / kBucketThreads], bk[N2 / kBucketThreads];
+#pragma unroll
+    for (int i = 0; i < N2 / kBucketThreads; ++i) {
+      const int e = tid + i * kBucketThreads;
+      if (e < n) {
+        const int b = min(NB - 1, (int)((float)(raw[e] - kmin) * scale));
+        bk[i] = b;
+        slot[i] = atomicAdd(&cnt[b], 1);
+      }
+    }
+    __syncthreads();
+    // exclusive scan of the NB counters (each thread NB/128 consecutive ones), largest bucket
+    constexpr int PER = NB / kBucketThreads;
+    int loc[PER], sum = 0, mb = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      loc[i] = cnt[tid * PER + i];
+      mb = max(mb, loc[i]);
+      sum += loc[i];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    if (lane == 31) red[warp][0] = (uint32_t)incl;
+    if (lane == 0) atomicMax(&maxb, mb);
+    __syncthreads();
+    int base = incl - sum;
+    for (int w = 0; w < warp; ++w) base += (int)red[w][0];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      cnt[tid * PER + i] = base;
+      base += loc[i];
+    }
+    if (tid == kBucketThreads - 1) cnt[NB] = n;
+    __syncthreads();
+    const bool fallback = maxb > kMaxBucket;
+    if (!fallback) {
+#pragma unroll
+      for (int i = 0; i < N2 / kBucketThreads; ++i) {
+        const int e = tid + i * kBucketThreads;
+        if (e < n) {
+          const int q = cnt[bk[i]] + slot[i];
+          key[q] = raw[e];
+          idx[q] = (uint16_t)e;
+        }
+      }
+      __syncthreads();
+      // final position of each key: its bucket's start + its rank inside the bucket (smaller keys,
+      // then equal keys at lower slots) -- independent per key, no sequential insertion
+#pragma unroll
+      for (int i = 0; i < N2 / kBucketThreads; ++i) {
+        const int e = tid + i * kBucketThreads;
+        if (e < n) {
+          const int lo = cnt[bk[i]], hi = cnt[bk[i] + 1], q = lo + slot[i];
+          const uint32_t kv = raw[e];
+          int rank = 0;
+          for (int j = lo; j < hi; ++j) {
+            const uint32_t kj = key[j];
+            rank += (kj < kv || (kj == kv && j < q)) ? 1 : 0;
+          }
+          sk[lo + rank] = kv;
+          si[lo + rank] = (uint16_t)e;
+        }
+      }
+    } else {
+      // a stretched row: block bitonic network over N2 slots (+inf-key padding sorts last)
+      for (int e = tid; e < N2; e += kBucketThreads) {
+        key[e] = e < n ? raw[e] : 0xFFFFFFFFu;
+        idx[e] = (uint16_t)(e < n ? e : 0xFFFF);
+      }
+      __syncthreads();
+      for (int size = 2; size <= N2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int c = tid; c < (N2 >> 1); c += kBucketThreads) {
+            const int lo = 2 * c - (c & (stride - 1));
+            const int hi = lo + stride;
+            const bool asc = (lo & size) == 0;
+            const uint32_t a = key[lo], b = key[hi];
+            if ((a > b) == asc) {
+              key[lo] = b;
+              key[hi] = a;
+              const uint16_t t = idx[lo];
+              idx[lo] = idx[hi];
+              idx[hi] = t;
+            }
+          }
+          __syncthreads();
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t* ok_ = fallback ? key : sk;
+    const uint16_t* oi_ = fallback ? idx : si;
+    for (int e = tid; e < n_pad; e += kBucketThreads) {
+      S[p * n_pad + e] = e < n ? key_float(ok_[e]) : INFINITY;
+      perm[p * n_pad + e] = e < n ? oi_[e] : (uint16_t)0xFFFF;
+    }
+    __syncthreads();  // smem reused by the next row
+  }
+}
+
+template <int NB, int N2>
+cudaError_t launch_sort_bucket(corr_field* f, cudaStream_t st) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sort_bucket_kernel<NB, N2>, kBucketThreads, 0);
+  if (occ < 1) occ = 1;
+  int64_t blocks = (int64_t)kSMs * occ * 4;
+  if (blocks > f->P) blocks = f->P;
+  sort_bucket_kernel<NB, N2><<<(unsigned)blocks, kBucketThreads, 0, st>>>(f->F, f->S, f->perm, f->n, f->n_pad, f->P);
+  return cudaSuccess;
+}
+
 template <int T, int I>
 cudaError_t launch_sort_radix(corr_field* f, cudaStream_t st) {
   int occ = 0;
@@ -310,15 +487,30 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
     while ((1 << log2n2) < f->n) ++log2n2;
     const int N2 = 1 << log2n2;
     cudaError_t er = cudaErrorInvalidValue;
-    switch (N2) {
-      case 64: er = launch_sort_radix<32, 2>(f, st); break;
-      case 128: er = launch_sort_radix<32, 4>(f, st); break;
-      case 256: er = launch_sort_radix<64, 4>(f, st); break;
-      case 512: er = launch_sort_radix<64, 8>(f, st); break;
-      case 1024: er = launch_sort_radix<64, 16>(f, st); break;
-      case 2048: er = launch_sort_radix<256, 8>(f, st); break;
-      case 4096: er = launch_sort_radix<256, 16>(f, st); break;
-      default: break;
+    static const bool radix = [] {  // A/B switch: the round-1 CUB radix sort
+      const char* v = getenv("CORR_SORT_RADIX");
+      return v && v[0] == '1';
+    }();
+    if (radix || N2 > 1024) {  // n > 1024: the radix sort (the bucket kernel's static smem is for n <= 1024)
+      switch (N2) {
+        case 64: er = launch_sort_radix<32, 2>(f, st); break;
+        case 128: er = launch_sort_radix<32, 4>(f, st); break;
+        case 256: er = launch_sort_radix<64, 4>(f, st); break;
+        case 512: er = launch_sort_radix<64, 8>(f, st); break;
+        case 1024: er = launch_sort_radix<64, 16>(f, st); break;
+        case 2048: er = launch_sort_radix<256, 8>(f, st); break;
+        case 4096: er = launch_sort_radix<256, 16>(f, st); break;
+        default: break;
+      }
+    } else {
+      switch (N2) {  // NB = 2 N2 buckets: about 0.5 keys per bucket, so the per-bucket sorts stay short
+        case 64:
+        case 128:
+        case 256: er = launch_sort_bucket<512, 256>(f, st); break;
+        case 512: er = launch_sort_bucket<1024, 512>(f, st); break;
+        case 1024: er = launch_sort_bucket<2048, 1024>(f, st); break;
+        default: break;
+      }
     }
     if (er == cudaSuccess) {
       note_launch(2);
