@@ -386,6 +386,25 @@ def main():
                           "frac": (hi - lo) * Sd * n * (n - 1) / dense_s / peak,
                           "executed_comparisons_per_pair": dense_exec / max((hi - lo) * Sd, 1),
                           "pairs_per_s": (hi - lo) * Sd / dense_s, "sample": f"{hi - lo} region pairs x {Sd} samples"}
+    # the round-1 formulation (x-sorted block sweep, CORR_F_KSG_SWEEP) on the same subset: it executes
+    # ~15x more comparisons at a higher fraction of the comparison peak but fewer pairs/s -- the
+    # reference that shows what the cell k-NN's lower executed-comparison fraction buys
+    roofline_sweep = None
+    if not args.no_dense:
+        Sd = 256
+        cb.corr_ksg_comparisons(local, reset=True)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        cb.corr_region_max(field, None, cb.CORR_KSG | cb.CORR_F_KSG_SWEEP, K_NN, Ash, Bsh, Sd, SEED)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        sw_s = d0.elapsed_time(d1) / 1e3
+        sw_exec = cb.corr_ksg_comparisons(local, reset=True)
+        roofline_sweep = {"bound": "alu", "kernel": "ksg_sorted_kernel<3,1,4,sweep> (round-1 x-sorted block sweep)",
+                          "achieved": sw_exec / sw_s / 1e9, "peak": peak / 1e9, "unit": "Gcmp/s",
+                          "frac": sw_exec / sw_s / peak,
+                          "executed_comparisons_per_pair": sw_exec / max((hi - lo) * Sd, 1),
+                          "pairs_per_s": (hi - lo) * Sd / sw_s, "sample": f"{hi - lo} region pairs x {Sd} samples"}
     # secondary: the focus-block GEMM (tensor-bound) and the sampled Pearson pairs (HBM/L2-bound)
     fa_box, fb_box = slabs[rank], fB
     nA = (fa_box[3] - fa_box[0]) * (fa_box[4] - fa_box[1]) * (fa_box[5] - fa_box[2])
@@ -515,7 +534,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, args, world),
-                "roofline": roofline, "roofline_ksg_dense": roofline_dense, "roofline_pearson_block": roofline_block,
+                "roofline": roofline, "roofline_ksg_sweep": roofline_sweep, "roofline_ksg_dense": roofline_dense, "roofline_pearson_block": roofline_block,
                 "roofline_pearson_pairs": roofline_pearson_pairs, "cpu_baseline": cpu_base, "e2e": e2e, "clocks": clk,
                 "gpu_launches": launches, "field_create_s": create_s,
                 "ingest": {"bound": "hbm", "kernels": "transpose_kernel + stats_kernel + sort_radix_kernel",

@@ -47,8 +47,10 @@ enum {
   CORR_F_KSG_PLUS1 = 1 << 8, /* KSG with psi(n_x+1), psi(n_y+1) (Kraskov alg. 1; reading R1) */
   CORR_F_ABS = 1 << 9,       /* region max of |value| (reading R11)           */
   CORR_F_KSG_DENSE = 1 << 10, /* KSG: evaluate all n(n-1) comparisons (no pruning); same results  */
-  CORR_F_KSG_COUNT = 1 << 11  /* KSG: tally executed comparisons for corr_ksg_comparisons (slower; */
+  CORR_F_KSG_COUNT = 1 << 11, /* KSG: tally executed comparisons for corr_ksg_comparisons (slower; */
                               /* same results) -- a diagnostic for the roofline report          */
+  CORR_F_KSG_SWEEP = 1 << 12  /* KSG: the round-1 x-sorted block sweep instead of the column-cell */
+                              /* k-NN (same results) -- the bench's reference formulation        */
 };
 enum { CORR_OK = 0, CORR_E_INVAL = -1, CORR_E_RANGE = -2, CORR_E_NOMEM = -3, CORR_E_CUDA = -4 };
 

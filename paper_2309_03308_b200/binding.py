@@ -22,6 +22,7 @@ CORR_F_KSG_PLUS1 = 1 << 8
 CORR_F_ABS = 1 << 9
 CORR_F_KSG_DENSE = 1 << 10
 CORR_F_KSG_COUNT = 1 << 11
+CORR_F_KSG_SWEEP = 1 << 12
 CORR_OK, CORR_E_INVAL, CORR_E_RANGE, CORR_E_NOMEM, CORR_E_CUDA = 0, -1, -2, -3, -4
 
 EXPORTS = ("corr_field_create", "corr_field_update", "corr_field_aggregate", "corr_field_destroy", "corr_field_info", "corr_eval_pairs",

@@ -125,7 +125,10 @@ int alloc_field(int32_t nx, int32_t ny, int32_t nz, int32_t members, int32_t dev
 }
 
 bool ksg_plus1(int32_t measure) { return (measure & CORR_F_KSG_PLUS1) != 0; }
-KsgPath ksg_path(int32_t measure) { return (measure & CORR_F_KSG_DENSE) ? kKsgDense : kKsgAuto; }
+KsgPath ksg_path(int32_t measure) {
+  if (measure & CORR_F_KSG_DENSE) return kKsgDense;
+  return (measure & CORR_F_KSG_SWEEP) ? kKsgSweep : kKsgAuto;
+}
 
 // Host-input staging of a field: two device slices of kStageMembers members each, a copy stream
 // and the events ordering copies against transposes.  Created on the first host upload, kept for
@@ -206,7 +209,7 @@ int check_pair_fields(const corr_field* fa, const corr_field*& fb) {
 int resolve_k(const corr_field* f, int32_t measure, int32_t& k) {
   const int kind = measure & 0xFF;
   if (kind != CORR_PEARSON && kind != CORR_KSG) return fail(CORR_E_INVAL, "unknown measure kind");
-  if (measure & ~(0xFF | CORR_F_KSG_PLUS1 | CORR_F_ABS | CORR_F_KSG_DENSE | CORR_F_KSG_COUNT))
+  if (measure & ~(0xFF | CORR_F_KSG_PLUS1 | CORR_F_ABS | CORR_F_KSG_DENSE | CORR_F_KSG_COUNT | CORR_F_KSG_SWEEP))
     return fail(CORR_E_INVAL, "unknown measure flags");
   if (kind == CORR_PEARSON) {
     k = 0;

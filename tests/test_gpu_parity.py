@@ -340,7 +340,8 @@ def test_invariances_on_gpu_path():
 
 
 def test_dense_and_sweep_identical():
-    """The exact sweep (default) and CORR_F_KSG_DENSE give bit-identical results."""
+    """The column-cell k-NN (default), the round-1 sweep (CORR_F_KSG_SWEEP), the counting build
+    (CORR_F_KSG_COUNT) and CORR_F_KSG_DENSE give bit-identical results."""
     spec = synth.spec_of(synth.C4)
     vals, f = _field(spec)
     del vals
@@ -349,7 +350,11 @@ def test_dense_and_sweep_identical():
     for k in (3, 30):
         m1, a1 = cb.corr_region_max(f, None, cb.CORR_KSG, k, A, B, 8, 5)
         m2, a2 = cb.corr_region_max(f, None, cb.CORR_KSG | cb.CORR_F_KSG_DENSE, k, A, B, 8, 5)
+        m3, a3 = cb.corr_region_max(f, None, cb.CORR_KSG | cb.CORR_F_KSG_SWEEP, k, A, B, 8, 5)
+        m4, a4 = cb.corr_region_max(f, None, cb.CORR_KSG | cb.CORR_F_KSG_COUNT, k, A, B, 8, 5)
         assert torch.equal(m1, m2) and torch.equal(a1, a2)
+        assert torch.equal(m1, m3) and torch.equal(a1, a3)  # column-cell k-NN == round-1 sweep
+        assert torch.equal(m1, m4) and torch.equal(a1, a4)  # the counting build: same results
     f.close()
 
 
