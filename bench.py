@@ -185,7 +185,8 @@ def config_dict(cfg, args, world):
                         f"(+ Pearson sampled region max + Pearson exhaustive focus block)",
             "grid": [cfg.nx, cfg.ny, cfg.nz], "members": cfg.members, "k": K_NN, "region_pairs": 3828,
             "samples_per_region_pair": args.samples, "parallelism": f"region-pair shards x{world}",
-            "l2": "inputs larger than L2 (field rows 7 GB x planes, random rows per pair)"}
+            "l2": "inputs larger than L2 (field rows 7 GB x planes, random rows per pair)",
+            "limits": "members <= 4096; KSG k in [1, n-1] (k >= 33: multi-pass lists); exhaustive |A||B| < 2^32"}
 
 
 # --------------------------------------------------------------------------- our arm

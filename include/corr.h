@@ -132,7 +132,10 @@ int corr_eval_pairs(const corr_field* fa, const corr_field* fb, int32_t measure,
  *                      results.  Ties -> lowest sample index s.
  *   samples == 0     : every one of the |A|*|B| pairs (exhaustive).  Ties ->
  *                      lowest q = a_local*|B| + b_local (local index x fastest in a box).
- *                      Pearson uses the tcgen05 split-TF32 block GEMM with a fused max.
+ *                      Pearson uses the tcgen05 split-TF32 block GEMM with a fused max; boxes
+ *                      the GEMM's TMA tiling cannot map (deeper than 256 grid layers in z) run
+ *                      on the CUDA-core pair path instead (same results, slower; such calls
+ *                      add nothing to corr_gemm_flops).
  *   out_max          : DEVICE float32 [R]; NaN if every evaluated value was NaN.
  *   out_argmax       : DEVICE int64 [R][2] = (point in A, point in B), (-1,-1) if none.
  * NaN values are skipped.  With one field (fb == NULL) the self pair (a, a) is skipped
