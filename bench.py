@@ -291,10 +291,9 @@ def main():
             ev["pearson_sampled"].append((t1, t2))
             ev["pearson_block"].append((t2, t3))
         if world > 1:
-            km, ka = cdist.gather_region_results(km, ka, bounds)
-            pm, pa = cdist.gather_region_results(pm, pa, bounds)
-            # the focus pair's slabs: one all-reduce MAX over packed (value, q) keys, on the device
-            fm, fa = cdist.combine_focus_device(fm, fa, slabs, fB, spec.nx, spec.ny)
+            # all-gathers of the shards' region maxima + one all-reduce MAX over the focus slabs'
+            # packed (value, q) keys, on the device (tests/test_dist.py runs it under gloo)
+            km, ka, pm, pa, fm, fa = cdist.combine_step(km, ka, pm, pa, fm, fa, bounds, slabs, fB, spec.nx, spec.ny)
         return km, ka, pm, pa, fm, fa
 
     for _ in range(args.warmup):

@@ -175,3 +175,13 @@ def combine_focus_device(fm: torch.Tensor, fa: torch.Tensor, slabs, boxB, nx: in
     else:
         tdist.all_reduce(key, op=tdist.ReduceOp.MAX, group=group)
     return decode_focus_key(key, slabs, boxB, nx, ny)
+
+
+def combine_step(km, ka, pm, pa, fm, fa, bounds, slabs, boxB, nx: int, ny: int, group=None):
+    """The exchange step of one bench step: every rank holds its shard's
+    KSG and Pearson region maxima and its focus slab's maximum; afterwards every rank holds the
+    full results -- one all-gather per measure, one all-reduce MAX for the focus pair."""
+    km, ka = gather_region_results(km, ka, bounds, group=group)
+    pm, pa = gather_region_results(pm, pa, bounds, group=group)
+    fm, fa = combine_focus_device(fm, fa, slabs, boxB, nx, ny, group=group)
+    return km, ka, pm, pa, fm, fa

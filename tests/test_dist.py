@@ -109,3 +109,52 @@ def test_focus_key_order_and_roundtrip():
     k0 = cdist.focus_key(torch.tensor([-0.0]), fa[2:3], slabs, boxB, nx, ny)
     k1 = cdist.focus_key(torch.tensor([0.0]), fa[2:3], slabs, boxB, nx, ny)
     assert torch.equal(k0, k1)                             # ... same pair: identical keys
+
+
+def _step_worker(rank, world, port, q):
+    """bench.py's per-step orchestration (dist.combine_step) with the per-rank results computed by
+    the oracle on the rank's shard / focus slab."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    spec = synth.spec_of(synth.C1)
+    f = synth.generate(spec).numpy()
+    A, B = synth.context_pairs(synth.bricks_of(synth.C1))
+    bounds = cdist.shard_bounds([30] * len(A), world)
+    lo, hi = bounds[rank]
+    km, ka = oracle.region_max(f, None, (8, 8, 4), oracle.KSG, 3, A[lo:hi], B[lo:hi], 30, 7)
+    pm, pa = oracle.region_max(f, None, (8, 8, 4), oracle.PEARSON, 0, A[lo:hi], B[lo:hi], 30, 7)
+    FA, FB = (0, 0, 0, 8, 4, 4), (0, 4, 0, 8, 8, 4)
+    slabs = cdist.split_box_z(FA, world)
+    fm, fa = oracle.region_max(f, None, (8, 8, 4), oracle.PEARSON, 0, [slabs[rank]], [FB], 0, 0)
+    t = lambda a, dt: torch.from_numpy(np.asarray(a).astype(dt))  # noqa: E731
+    out = cdist.combine_step(t(km, np.float32), t(ka, np.int64), t(pm, np.float32), t(pa, np.int64),
+                             t(fm, np.float32), t(fa, np.int64), bounds, slabs, FB, 8, 8)
+    q.put((rank, [o.numpy() for o in out]))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_bench_step_orchestration(world):
+    """The bench step's exchange (all-gathers + focus all-reduce MAX) reproduces the single-process
+    results bit for bit on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spec = synth.spec_of(synth.C1)
+    f = synth.generate(spec).numpy()
+    A, B = synth.context_pairs(synth.bricks_of(synth.C1))
+    km, ka = oracle.region_max(f, None, (8, 8, 4), oracle.KSG, 3, A, B, 30, 7)
+    pm, pa = oracle.region_max(f, None, (8, 8, 4), oracle.PEARSON, 0, A, B, 30, 7)
+    fm, fa = oracle.region_max(f, None, (8, 8, 4), oracle.PEARSON, 0, [(0, 0, 0, 8, 4, 4)], [(0, 4, 0, 8, 8, 4)], 0, 0)
+    for _, out in res:
+        assert np.array_equal(out[0], km.astype(np.float32)) and np.array_equal(out[1], ka)
+        assert np.array_equal(out[2], pm.astype(np.float32)) and np.array_equal(out[3], pa)
+        assert out[4][0] == np.float32(fm[0]) and tuple(out[5][0]) == tuple(fa[0])
