@@ -312,12 +312,36 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 8 : 4)) ksg_cell_kernel(
         int nb = 0;
         if (lane == 0) nb = atomicAdd(next_blk, 1);  // claim the next column (latency hides below)
         // ---- a4 / a5: strict marginal counts (binary searches on the sorted rows) and psi ----
+        // The strips |x - x_i| < eps and |y - y_i| < eps lie around the member's own ranks
+        // (t_i in the x row, s_i in the y row).  If, for every lane, both strips end within 127
+        // ranks of t_i / s_i on both sides (checked at the window edges with the same monotone
+        // predicates), 7-step searches over 128-wide windows replace the full log2(n)-step ones.
+        const float e = l[K - 1];
+        uint32_t xu = su_base, xw = su_base, yu = sv_base, yw = sv_base;
+        bool win_ok = true;
+        if (active && e > 0.f) {
+          const int si = (int)lds_u16(cols_base + (uint32_t)(c * 32 + lane) * 2u);
+          const int ti = xr[pv_s[si]];
+          const int bxw = max(0, ti - 127), bxu = min(ti, L.nsx - 128);
+          const int byw = max(0, si - 127), byu = min(si, L.nsx - 128);
+          win_ok = (bxw == 0 || !(zi.x - su[bxw - 1] < e)) && (su[bxu + 127] - zi.x >= e) &&
+                   (byw == 0 || !(zi.y - sv[byw - 1] < e)) && (sv[byu + 127] - zi.y >= e);
+          xw = su_base + (uint32_t)bxw * 4u;
+          xu = su_base + (uint32_t)bxu * 4u;
+          yw = sv_base + (uint32_t)byw * 4u;
+          yu = sv_base + (uint32_t)byu * 4u;
+        }
+        const bool windowed = __all_sync(0xffffffffu, win_ok);
         if (active) {
-          const float e = l[K - 1];
           int cx = 0, cy = 0;
           if (e > 0.f) {
-            uint32_t xu = su_base, xw = su_base, yu = sv_base, yw = sv_base;
-            CountSearch44<12>::run(L.log2p, xu, xw, yu, yw, zi.x, zi.y, e);
+            if (windowed) {
+              CountSearch44<6>::run(7, xu, xw, yu, yw, zi.x, zi.y, e);
+            } else {
+              xu = xw = su_base;
+              yu = yw = sv_base;
+              CountSearch44<12>::run(L.log2p, xu, xw, yu, yw, zi.x, zi.y, e);
+            }
             cx = (int)((xu - xw) >> 2) - 1;
             cy = (int)((yu - yw) >> 2) - 1;
           }
