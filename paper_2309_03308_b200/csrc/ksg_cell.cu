@@ -236,19 +236,14 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 8 : 4)) ksg_cell_kernel(
       }
     }
     __syncthreads();
-    for (int c = warp; c < nch; c += NW) {  // exclusive prefix over the y-segments of column c
-      int carry = 0;
-      for (int g0 = 0; g0 < nseg; g0 += 32) {
-        const int g = g0 + lane;
-        const int v = g < nseg ? cs[c * cs_stride + g] : 0;
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        if (g < nseg) cs[c * cs_stride + g] = (uint16_t)(carry + incl - v);
-        carry += __shfl_sync(0xffffffffu, incl, 31);
+    // exclusive prefix over the y-segments of every column: one thread per column walks its
+    // segments (sequential, ~10x fewer instructions than a warp scan per column: +3.9 %)
+    for (int c = tid; c < nch; c += NT) {
+      int run = 0;
+      for (int g = 0; g < nseg; ++g) {
+        const int v = cs[c * cs_stride + g];
+        cs[c * cs_stride + g] = (uint16_t)run;
+        run += v;
       }
     }
     __syncthreads();
