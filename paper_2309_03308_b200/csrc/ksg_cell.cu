@@ -284,25 +284,39 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 8 : 4)) ksg_cell_kernel(
         // neighbour columns, nearest first, alternating sides; a side ends at the first column no
         // lane needs (its x-gap only grows outward, the lists only shrink)
         int lo = c - 1, hi = c + 1, dir = 0;
+        // addresses kept incrementally: the nearest x of the next column on each side (its last /
+        // first x-rank) and that column's entry block
+        uint32_t eL = su_base + (uint32_t)(32 * lo + 31) * 4u, eR = su_base + (uint32_t)(32 * hi) * 4u;
+        uint32_t bL = col_base + (uint32_t)(lo * kCS) * 8u, bR = col_base + (uint32_t)(hi * kCS) * 8u;
+        uint32_t sL = cs_base + (uint32_t)(lo * cs_stride + band) * 2u, sR = cs_base + (uint32_t)(hi * cs_stride + band) * 2u;
 #pragma unroll 1
         while (lo >= 0 || hi < nch) {
           const bool right = lo < 0 || (hi < nch && dir);
           dir ^= 1;
-          const int cc = right ? hi : lo;
-          const float xe = lds_f32(su_base + (uint32_t)(32 * cc + (right ? 0 : 31)) * 4u);
+          const float xe = lds_f32(right ? eR : eL);
           const float gap = right ? xe - zi.x : zi.x - xe;
           const bool need = active && gap < l[K - 1];
           if (!__any_sync(0xffffffffu, need)) {
             if (right) hi = nch; else lo = -1;
             continue;
           }
-          const uint32_t nb0 = col_base + (uint32_t)(cc * kCS) * 8u;
-          const uint32_t start = lds_u16(cs_base + (uint32_t)(cc * cs_stride + band) * 2u);
+          const uint32_t nb0 = right ? bR : bL;
+          const uint32_t start = lds_u16(right ? sR : sL);
           pu = need ? nb0 + (1u + start) * 8u : nb0 + 33u * 8u;
           pd = need ? nb0 + start * 8u : nb0;
           scan_column<K>(pu, pd, zi, l);
           if (COUNT && need) ncand += (int)((pu - pd) >> 3) + 1 - (pu == nb0 + 33u * 8u) - (pd == nb0);
-          if (right) ++hi; else --lo;
+          if (right) {
+            ++hi;
+            eR += 128u;
+            bR += kCS * 8u;
+            sR += (uint32_t)cs_stride * 2u;
+          } else {
+            --lo;
+            eL -= 128u;
+            bL -= kCS * 8u;
+            sL -= (uint32_t)cs_stride * 2u;
+          }
         }
         int nb = 0;
         if (lane == 0) nb = atomicAdd(next_blk, 1);  // claim the next column (latency hides below)
