@@ -356,6 +356,21 @@ def main():
             ncu_ctx = {k: tr[k] for k in ("ksg_kernel", "alu_pipe_pct", "issue_active_pct", "source") if k in tr}
         except Exception:
             traffic = None
+    # the same kernel against the ALU pipe itself: ALU-pipe warp-instructions per pair measured by
+    # ncu on this workload (profiles/ncu_traffic.json) x the pairs of the timed launches, vs
+    # 148 SMs x 2 ALU warp-instr/clk -- how busy the hardware is, next to the algorithmic figure
+    roofline_alu = None
+    try:
+        alu_pp = json.load(open(NCU_TRAFFIC)).get("alu_warp_instr_per_pair")
+    except Exception:
+        alu_pp = None
+    if alu_pp:
+        alu_peak = 148 * 2 * sm_max * 1e6
+        alu_ach = alu_pp * my_pairs / (ksg_ms / 1e3)
+        roofline_alu = {"bound": "alu", "kernel": f"ksg_cell_kernel<{K_NN},4>", "unit": "ALU warp-instr/s",
+                        "achieved": alu_ach, "peak": alu_peak, "frac": alu_ach / alu_peak,
+                        "per_pair": alu_pp, "per_pair_source": "ncu sm__inst_executed_pipe_alu of the same "
+                                                                "kernel on this workload (profiles/ncu_traffic.json)"}
     roofline = {"bound": "alu", "kernel": f"ksg_cell_kernel<{K_NN},4> (column-cell k-NN + counts + psi)",
                 "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcmp/s", "frac": achieved / peak,
                 "traffic": traffic,
@@ -534,7 +549,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, args, world),
-                "roofline": roofline, "roofline_ksg_sweep": roofline_sweep, "roofline_ksg_dense": roofline_dense, "roofline_pearson_block": roofline_block,
+                "roofline": roofline, "roofline_alu_pipe": roofline_alu, "roofline_ksg_sweep": roofline_sweep, "roofline_ksg_dense": roofline_dense, "roofline_pearson_block": roofline_block,
                 "roofline_pearson_pairs": roofline_pearson_pairs, "cpu_baseline": cpu_base, "e2e": e2e, "clocks": clk,
                 "gpu_launches": launches, "field_create_s": create_s,
                 "ingest": {"bound": "hbm", "kernels": "transpose_kernel + stats_kernel + sort_radix_kernel",
