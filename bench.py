@@ -471,7 +471,10 @@ def main():
         host = torch.empty((spec.members, spec.points), dtype=torch.float32, pin_memory=True)
         host.copy_(vals)
         slots = [field, cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members, device=local)]
-        up = torch.cuda.Stream()
+        # the update runs on a HIGH-priority stream: the step's KSG grid is one pair per CTA (15.7 M
+        # CTAs), and without priority the update's transposes would be dispatched only after all of
+        # them, stalling the slice ring of the streamed upload until the step ends
+        up = torch.cuda.Stream(priority=-1)
         h2d = spec.members * spec.points * 4
         d2h_holder = [0]
         pinned_out = None

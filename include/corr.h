@@ -88,7 +88,9 @@ int corr_field_aggregate(const corr_field* f, int32_t fx, int32_t fy, int32_t fz
  * cudaMemcpyAsync each on the field's own copy stream into two persistent device slices (allocated
  * on the first host update, 2 x 32 x P x 4 bytes) and each slice is transposed on `cuda_stream` as
  * soon as it has landed; page-locked (pinned) memory makes the copies overlap device work.  The
- * host buffer must stay unchanged until `cuda_stream` has passed this call's work.  Calls on
+ * host buffer must stay unchanged until `cuda_stream` has passed this call's work.  To overlap an
+ * update with compute on another stream, pass a HIGH-priority stream here: the pair kernels launch
+ * one pair per CTA, and a normal-priority stream's transposes would wait behind all of them.  Calls on
  * other streams that still read the field must be ordered before it by the caller (events).
  * A non-finite value is detected on the device: the next corr_check() returns CORR_E_INVAL (the
  * field content is undefined until the next clean update).

@@ -3,6 +3,7 @@
 // computation runs in the kernels of field.cu / ksg.cu / pearson.cu /
 // pearson_gemm.cu; without a usable CUDA device calls return CORR_E_CUDA.
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -15,6 +16,14 @@
 using namespace corr;
 
 std::atomic<long long> corr::g_launch_count{0};
+
+int corr::grid_waves_env() {
+  static const int w = [] {
+    const char* v = getenv("CORR_WAVES");
+    return v ? atoi(v) : -1;  // -1: not set
+  }();
+  return w;
+}
 
 namespace {
 

@@ -38,6 +38,13 @@ struct corr_field {
 namespace corr {
 
 constexpr int kSMs = 148;
+
+// Grid size of the pair kernels: `waves` CTAs per resident CTA slot, each CTA looping over its
+// pair units with a grid stride.  Measured (round 2, ksg_cell_kernel, C4): one persistent wave
+// 2.14e7 pairs/s, 16 waves 2.48e7, one unit per CTA 2.52e7 -- the hardware block scheduler's
+// dynamic assignment and staggered CTA phases beat a static grid-stride split.  The environment
+// variable CORR_WAVES overrides (A/B); <= 0 means one unit per CTA.
+int grid_waves_env();
 extern std::atomic<long long> g_launch_count;  // kernels launched (corr_launch_count)
 inline void note_launch(int k = 1) { g_launch_count.fetch_add(k, std::memory_order_relaxed); }
 

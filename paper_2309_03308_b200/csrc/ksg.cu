@@ -733,8 +733,10 @@ cudaError_t launch_t(const corr_field* fa, const corr_field* fb, int k, int plus
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);
   if (occ < 1) occ = 1;
   int64_t blocks = src.nunits;
-  const int64_t cap = (int64_t)kSMs * occ;
-  if (blocks > cap) blocks = cap;
+  // one pair unit per CTA (grid_waves_env): +11 % over a persistent wave for the sweep at C4
+  const int waves = grid_waves_env() == -1 ? 0 : grid_waves_env();
+  if (waves > 0 && blocks > (int64_t)kSMs * occ * waves) blocks = (int64_t)kSMs * occ * waves;
+  if (blocks > 0x7FFFFFFF) blocks = 0x7FFFFFFF;
   kern<<<(unsigned)blocks, warps * 32, smem, st>>>(fa->S, fa->perm, fa->F, fb->S, fb->perm, fb->F, fa->spread,
                                                    fb->spread, fa->cflag, fb->cflag, fa->psi, n, n_pad, k, plus1 & 1,
                                                    src, out);
@@ -887,8 +889,11 @@ cudaError_t launch_warp(const corr_field* fa, const corr_field* fb, int k, int p
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
   if (occ < 1) occ = 1;
   int64_t blocks = (src.nunits + 3) / 4;
-  const int64_t cap = (int64_t)kSMs * occ;
-  if (blocks > cap) blocks = cap;
+  // 32 waves of warps looping over pairs (keeps each warp's two-slot staging pipeline, adds the
+  // block scheduler's balancing): +13 % over one persistent wave at C3 (grid_waves_env)
+  const int waves = grid_waves_env() == -1 ? 32 : grid_waves_env();
+  if (waves > 0 && blocks > (int64_t)kSMs * occ * waves) blocks = (int64_t)kSMs * occ * waves;
+  if (blocks > 0x7FFFFFFF) blocks = 0x7FFFFFFF;
   kern<<<(unsigned)blocks, 128, smem, st>>>(fa->S, fa->perm, fa->F, fb->S, fb->perm, fb->F, fa->spread, fb->spread,
                                             fa->cflag, fb->cflag, fa->psi, n, n_pad, k, plus1 & 1, src, out);
   note_launch();

@@ -27,6 +27,8 @@
 //   candidate (re-merging a value >= l[k-1] is a no-op).
 //
 // Counts (a4) are the round-1 binary searches on the two sorted rows; psi / reduction as before.
+#include <stdlib.h>
+
 #include "ksg_common.cuh"
 
 namespace corr {
@@ -400,10 +402,18 @@ cudaError_t launch_cell_t(const corr_field* fa, const corr_field* fb, int k, boo
   if (e != cudaSuccess) return e;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, L.bytes);
+  static const int occ_cap = [] {  // A/B switch: resident CTAs per SM
+    const char* v = getenv("CORR_KSG_OCC");
+    return v ? atoi(v) : 0;
+  }();
+  if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;
   if (occ < 1) occ = 1;
+  // one pair unit per CTA by default (grid_waves_env, corr_internal.cuh): +18 % over a
+  // persistent grid-stride wave at C4
   int64_t blocks = src.nunits;
-  const int64_t cap = (int64_t)kSMs * occ;
-  if (blocks > cap) blocks = cap;
+  const int waves = grid_waves_env();
+  if (waves > 0 && blocks > (int64_t)kSMs * occ * waves) blocks = (int64_t)kSMs * occ * waves;
+  if (blocks > 0x7FFFFFFF) blocks = 0x7FFFFFFF;
   kern<<<(unsigned)blocks, NW * 32, L.bytes, st>>>(fa->S, fa->perm, fb->S, fb->perm, fa->spread, fb->spread, fa->cflag,
                                                    fb->cflag, fa->psi, fa->n, fa->n_pad, k, plus1 ? 1 : 0, src, out);
   note_launch();
