@@ -231,8 +231,10 @@ cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, con
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
     if (occ < 1) occ = 1;
     int64_t blocks = (src.nunits + 8 * ppw - 1) / (8 * ppw);
-    const int64_t cap = (int64_t)kSMs * occ * 4;
-    return (unsigned)(blocks > cap ? cap : blocks);
+    const int w = grid_waves_env() == -1 ? 64 : grid_waves_env();  // 64 waves: -2.5 % time vs 4 (A/B: CORR_WAVES)
+    const int64_t cap = w > 0 ? (int64_t)kSMs * occ * w : blocks;
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks > 0x7FFFFFFF ? 0x7FFFFFFF : blocks);
   };
   if (src.mode != kList && !noscreen) {
     // screened (exact) region max: bf16 pass over every pair, fp32 pass over the candidates
