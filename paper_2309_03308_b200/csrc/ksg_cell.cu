@@ -109,11 +109,19 @@ __device__ __forceinline__ bool scan_step(uint32_t& pu, uint32_t& pd, float2 zi,
   const float2 zu = lds_f2(pu), zd = lds_f2(pd);
   const float2 du = sub2(zi, zu), dd = sub2(zi, zd);
   merge2<K>(l, chebd(du), chebd(dd));
-  const bool su = -du.y >= l[K - 1];  // fl(y_j - y_i) = -fl(y_i - y_j) exactly
-  const bool sd = dd.y >= l[K - 1];
-  pu += su ? 0u : 8u;
-  pd -= sd ? 0u : 8u;
-  return __all_sync(0xffffffffu, su && sd);
+  // stop tests fused with the predicated pointer steps (fl(y_j - y_i) = -fl(y_i - y_j) exactly);
+  // written in PTX so each pointer moves in place (+1.0 % over the compiler's select + copy)
+  uint32_t both;
+  asm("{\n\t.reg .pred ps, pt, pb;\n\t"
+      "setp.ge.f32 ps, %3, %5;\n\t"
+      "setp.ge.f32 pt, %4, %5;\n\t"
+      "@!ps add.u32 %0, %0, 8;\n\t"
+      "@!pt sub.u32 %1, %1, 8;\n\t"
+      "and.pred pb, ps, pt;\n\t"
+      "selp.u32 %2, 1, 0, pb;\n\t}"
+      : "+r"(pu), "+r"(pd), "=r"(both)
+      : "f"(-du.y), "f"(dd.y), "f"(l[K - 1]));
+  return __all_sync(0xffffffffu, both != 0u);
 }
 
 template <int K>
