@@ -223,3 +223,21 @@ def _block_max_two_grids(xa, xb):
     mx, ab, sec = oracle.pearson_block_max(both, None, dims, (0, 0, 0, na, 1, 1), (na, 0, 0, na + nb, 1, 1),
                                            runner_up=True)
     return mx, (ab[0], ab[1] - na), sec
+
+
+def test_c4_paper_k_rule_all_region_pairs():
+    """C4 with the paper's k = ceil(3n/100) = 30 (k = 0; batched 32-entry lists),
+    S = 64, all 3828 region pairs: every argmax is a sampled pair whose oracle value equals the GPU
+    max; one region pair enumerated in full with the margin rule."""
+    spec = synth.spec_of(synth.C4)
+    vals, f = _field(spec)
+    del vals
+    torch.cuda.empty_cache()
+    A, B = synth.context_pairs(synth.bricks_of(synth.C4))
+    k = -(-3 * spec.members // 100)
+    assert k == 30
+    m0, a0 = cb.corr_region_max(f, None, cb.CORR_KSG, 0, A, B, 64, BENCH_SEED)   # k = 0: the rule
+    m1, a1 = cb.corr_region_max(f, None, cb.CORR_KSG, k, A, B, 64, BENCH_SEED)
+    assert torch.equal(m0, m1) and torch.equal(a0, a1)
+    _check_all_argmax(spec, None, f, None, cb.CORR_KSG, k, A, B, 64, BENCH_SEED, KSG_TOL, [2000], 256)
+    f.close()
