@@ -572,3 +572,26 @@ def test_ksg_nan_pairs_counted(n):
     mx, arg, sec, value_at = oracle_region_reference(vals, None, (nx, ny, nz), oracle.KSG, 3, A, B, S, 5)
     assert_region_argmax(_cpu(gm), _cpu(ga), mx, arg, sec, KSG_TOL, value_at)
     f.close()
+
+
+def test_concurrent_streams_same_field():
+    """The field is immutable after creation (corr.h): region-max calls on two streams at once
+    (sharing the resident region table and its events) give the results of sequential calls."""
+    spec = synth.spec_of(synth.C3)
+    vals, f = _field(spec)
+    del vals
+    A, B = synth.context_pairs(synth.bricks_of(synth.C3))
+    A, B = A[:600], B[:600]
+    ref_k = cb.corr_region_max(f, None, cb.CORR_KSG, 3, A, B, 64, 3)
+    ref_p = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, A, B, 64, 4)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            got_k = cb.corr_region_max(f, None, cb.CORR_KSG, 3, A, B, 64, 3, stream=s1)
+        with torch.cuda.stream(s2):
+            got_p = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, A, B, 64, 4, stream=s2)
+        torch.cuda.synchronize()
+        assert torch.equal(got_k[0], ref_k[0]) and torch.equal(got_k[1], ref_k[1])
+        assert torch.equal(got_p[0], ref_p[0]) and torch.equal(got_p[1], ref_p[1])
+    f.close()
