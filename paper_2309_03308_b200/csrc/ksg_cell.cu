@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
         if (COUNT && active) ncand += (int)((pu - pd) >> 3) - (pu == cb0 + 33u * 8u) - (pd == cb0);
         // neighbour columns, nearest first, alternating sides; a side ends at the first column no
         // lane needs (its x-gap only grows outward, the lists only shrink)
-        int lo = c - 1, hi = c + 1, dir = 0;
+        int lo = c - 1, hi = c + 1;
         // addresses kept incrementally: the nearest x of the next column on each side (its last /
         // first x-rank) and that column's entry block
         uint32_t eL = su_base + (uint32_t)(32 * lo + 31) * 4u, eR = su_base + (uint32_t)(32 * hi) * 4u;
@@ -303,31 +303,38 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
         uint32_t sL = cs_base + (uint32_t)(lo * cs_stride + band) * 2u, sR = cs_base + (uint32_t)(hi * cs_stride + band) * 2u;
 #pragma unroll 1
         while (lo >= 0 || hi < nch) {
-          const bool right = lo < 0 || (hi < nch && dir);
-          dir ^= 1;
-          const float xe = lds_f32(right ? eR : eL);
-          const float gap = right ? xe - zi.x : zi.x - xe;
-          const bool need = active && gap < l[K - 1];
-          if (!__any_sync(0xffffffffu, need)) {
-            if (right) hi = nch; else lo = -1;
-            continue;
+          // left then right, each side's test and visit written out (no per-test side select)
+          if (lo >= 0) {
+            const bool need = active && (zi.x - lds_f32(eL) < l[K - 1]);
+            if (!__any_sync(0xffffffffu, need)) {
+              lo = -1;
+            } else {
+              const uint32_t start = lds_u16(sL);
+              pu = need ? bL + (1u + start) * 8u : bL + 33u * 8u;
+              pd = need ? bL + start * 8u : bL;
+              scan_column<K>(pu, pd, zi, l);
+              if (COUNT && need) ncand += (int)((pu - pd) >> 3) + 1 - (pu == bL + 33u * 8u) - (pd == bL);
+              --lo;
+              eL -= 128u;
+              bL -= kCS * 8u;
+              sL -= (uint32_t)cs_stride * 2u;
+            }
           }
-          const uint32_t nb0 = right ? bR : bL;
-          const uint32_t start = lds_u16(right ? sR : sL);
-          pu = need ? nb0 + (1u + start) * 8u : nb0 + 33u * 8u;
-          pd = need ? nb0 + start * 8u : nb0;
-          scan_column<K>(pu, pd, zi, l);
-          if (COUNT && need) ncand += (int)((pu - pd) >> 3) + 1 - (pu == nb0 + 33u * 8u) - (pd == nb0);
-          if (right) {
-            ++hi;
-            eR += 128u;
-            bR += kCS * 8u;
-            sR += (uint32_t)cs_stride * 2u;
-          } else {
-            --lo;
-            eL -= 128u;
-            bL -= kCS * 8u;
-            sL -= (uint32_t)cs_stride * 2u;
+          if (hi < nch) {
+            const bool need = active && (lds_f32(eR) - zi.x < l[K - 1]);
+            if (!__any_sync(0xffffffffu, need)) {
+              hi = nch;
+            } else {
+              const uint32_t start = lds_u16(sR);
+              pu = need ? bR + (1u + start) * 8u : bR + 33u * 8u;
+              pd = need ? bR + start * 8u : bR;
+              scan_column<K>(pu, pd, zi, l);
+              if (COUNT && need) ncand += (int)((pu - pd) >> 3) + 1 - (pu == bR + 33u * 8u) - (pd == bR);
+              ++hi;
+              eR += 128u;
+              bR += kCS * 8u;
+              sR += (uint32_t)cs_stride * 2u;
+            }
           }
         }
         int nb = 0;
