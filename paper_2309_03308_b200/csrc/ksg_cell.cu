@@ -194,27 +194,34 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
   const int off = plus1 ? 1 : 0;
   unsigned long long executed = 0, nan_pairs = 0;
 
+  int* flags_s = reinterpret_cast<int*>(smem + L.o_misc) + 1;  // this pair's flags (skip, swap, degenerate)
   for (int64_t u = blockIdx.x; u < src.nunits; u += gridDim.x) {
-    int64_t a, b, r;
-    uint32_t idx;
-    const bool ok = unit_pair(src, u, a, b, r, idx);
-    if (!ok) {
-      if (src.mode == kList && tid == 0) out.out[u] = NAN;
-      continue;
-    }
-    const bool degenerate = (ca[a] | cb[b]) != 0;
-    if (degenerate && out.dbg_eps == nullptr) {
-      if (src.mode == kList && tid == 0) out.out[u] = NAN;
-      else if (tid == 0) ++nan_pairs;
-      continue;
-    }
-    const bool swap = spb[b] > spa[a];  // x = the wider marginal
-    const float* Su = swap ? Sb + b * n_pad : Sa + a * n_pad;
-    const uint16_t* Pu = swap ? Pb + b * n_pad : Pa + a * n_pad;
-    const float* Sv = swap ? Sa + a * n_pad : Sb + b * n_pad;
-    const uint16_t* Pv = swap ? Pa + a * n_pad : Pb + b * n_pad;
+    // thread 0 alone resolves the pair (sampler, flags) and stages its rows; the others learn the
+    // flags after the first build barrier.  A skipped unit stages row 0 (valid addresses, unused).
+    int64_t a = 0, b = 0, r = 0;
+    uint32_t idx = 0;
     __syncthreads();  // the previous pair is done with every shared array
     if (tid == 0) {
+      const bool ok = unit_pair(src, u, a, b, r, idx);
+      int fl = 0;
+      if (!ok) {
+        fl = 1;
+        a = b = 0;
+        if (src.mode == kList) out.out[u] = NAN;
+      } else if ((ca[a] | cb[b]) != 0) {  // a constant series: NaN (R10)
+        fl = 4;
+        if (out.dbg_eps == nullptr) {
+          fl |= 1;
+          if (src.mode == kList) out.out[u] = NAN; else ++nan_pairs;
+        }
+      }
+      const bool swap = spb[b] > spa[a];  // x = the wider marginal
+      fl |= swap ? 2 : 0;
+      *flags_s = fl;
+      const float* Su = swap ? Sb + b * n_pad : Sa + a * n_pad;
+      const uint16_t* Pu = swap ? Pb + b * n_pad : Pa + a * n_pad;
+      const float* Sv = swap ? Sa + a * n_pad : Sb + b * n_pad;
+      const uint16_t* Pv = swap ? Pa + a * n_pad : Pb + b * n_pad;
       *next_blk = NW;  // columns 0 .. NW-1 are taken statically
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_expect(bar, 2u * row_bytes + row_bytes);
@@ -236,6 +243,9 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
     // ---- build: x-rank of every member, stable multisplit of the y order by column ----
     for (int t = tid; t < n; t += NT) xr[pu_s[t]] = (uint16_t)t;
     __syncthreads();
+    const int fl = *flags_s;
+    if (fl & 1) continue;  // uniform: skipped unit
+    const bool swap = (fl & 2) != 0, degenerate = (fl & 4) != 0;
     for (int g = warp; g < nseg; g += NW) {
       const int s = 32 * g + lane;
       const bool valid = s < n;
