@@ -26,7 +26,10 @@
 //   +inf) so a scan stops there without bounds checks, and a stopped direction stays on its stop
 //   candidate (re-merging a value >= l[k-1] is a no-op).
 //
-// Counts (a4) are the round-1 binary searches on the two sorted rows; psi / reduction as before.
+// Counts (a4) are binary searches on the two sorted rows (128-wide windows around the member's own
+// ranks when every lane's strips fit, else the whole row); psi / reduction as in ksg.cu.
+// Launch: one pair unit per CTA (the hardware block scheduler balances and staggers the CTAs:
+// +18 % over a persistent grid-stride wave).
 #include <stdlib.h>
 
 #include "ksg_common.cuh"
