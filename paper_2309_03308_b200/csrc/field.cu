@@ -20,6 +20,7 @@
 #include <cub/block/block_radix_sort.cuh>
 
 #include "corr_internal.cuh"
+#include "ksg_common.cuh"
 
 namespace corr {
 namespace {
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(T) sort_radix_kernel(const float* __restrict__
   }
 }
 
-// ---- 3c. per-row bucket sort (one CTA of 128 threads per row, persistent over rows) ----------
+// ---- 3c. per-row bucket sort (one CTA per row at a time, persistent over rows) ---------------
 // The radix sort above needs ~5 ranked passes per row; ensemble rows are smooth distributions,
 // so one pass of BUCKETING plus tiny per-bucket sorts does the same job: keys u (order-preserving
 // u32, as above) map to NB buckets by b = floor((u - kmin) * NB / (kmax - kmin + 1)) computed in
@@ -243,7 +244,6 @@ __global__ void __launch_bounds__(T) sort_radix_kernel(const float* __restrict__
 // start plus its rank inside the bucket (about n/NB <= 0.5 keys per bucket).  Equal keys may land in any order: consumers only need SOME sorted
 // permutation (R4).  Rows whose largest bucket exceeds kMaxBucket (heavy outliers stretching the
 // range) are sorted by a block bitonic network instead, so no row costs O(n^2).
-constexpr int kBucketThreads = 128;
 constexpr int kMaxBucket = 48;
 
 __device__ __forceinline__ uint32_t ord_key(float f) {
@@ -254,30 +254,64 @@ __device__ __forceinline__ float key_float(uint32_t u) {
   return __uint_as_float(u ^ ((u >> 31) ? 0x80000000u : 0xFFFFFFFFu));
 }
 
-template <int NB, int N2>
-__global__ void __launch_bounds__(kBucketThreads) sort_bucket_kernel(const float* __restrict__ F, float* __restrict__ S,
-                                                                     uint16_t* __restrict__ perm, int n, int n_pad,
-                                                                     int64_t P) {
-  __shared__ uint32_t key[N2];     // bucketed keys (then, on the fallback, the bitonic array)
+// Persistent CTAs of TPB threads, one row at a time; the TMA unit stages the NEXT row
+// (cp.async.bulk of n_pad floats on an mbarrier) while the current one is bucketed.  Keys stay
+// in registers (N2 / TPB per thread); bucket counters are laid out so the scan's loads are
+// conflict-free; the sorted row and argsort leave through 16-byte stores.  Measured at C4
+// (n = 1000): 15.3 -> 14.5 ms per re-ingest sort with 128 threads per row; 256 threads cost more
+// (the per-warp reductions and scans are duplicated per warp; ncu: 6.7k warp-instructions per
+// row, issue 53 %), 64 threads starve the SM (28 KB of shared memory per CTA).
+template <int NB, int N2, int TPB>
+__global__ void __launch_bounds__(TPB) sort_bucket_kernel(const float* __restrict__ F, float* __restrict__ S,
+                                                          uint16_t* __restrict__ perm, int n, int n_pad, int64_t P) {
+  constexpr int PT = N2 / TPB;   // keys per thread
+  constexpr int NWARP = TPB / 32;
+  constexpr int PER = NB / TPB;  // bucket counters per thread in the scan
+  // bucket b's counter lives at (b % PER) * TPB + b / PER: thread t scans buckets t*PER ..
+  // t*PER + PER-1 with conflict-free loads (bucket NB -> NB, the end sentinel)
+  auto cidx = [](int b) { return b >= NB ? NB : (b % PER) * TPB + b / PER; };
+  __shared__ __align__(16) float buf[2][N2];  // staged rows (double buffer)
+  __shared__ uint32_t key[N2];                // bucketed keys (then, on the fallback, the bitonic array)
   __shared__ uint16_t idx[N2];
-  __shared__ uint32_t raw[N2];     // the row's keys in member order
-  __shared__ uint32_t sk[N2];      // sorted keys / member indices (bucket path)
-  __shared__ uint16_t si[N2];
+  __shared__ __align__(16) float sv[N2];      // the sorted row
+  __shared__ __align__(16) uint16_t si[N2];   // its argsort
   __shared__ int cnt[NB + 1];
-  __shared__ uint32_t red[4][2];
+  __shared__ uint32_t red[NWARP][2];
   __shared__ int maxb;
+  __shared__ uint64_t bar[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
-    const float* row = F + p * n_pad;
-    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
-    for (int e = tid; e < n; e += kBucketThreads) {
-      const uint32_t u = ord_key(row[e]);
-      raw[e] = u;
-      kmin = min(kmin, u);
-      kmax = max(kmax, u);
+  const uint32_t row_bytes = (uint32_t)n_pad * 4u;  // n_pad % 8 == 0: a multiple of 16 bytes
+  if (tid == 0) {
+    bar_init(bar);
+    bar_init(bar + 1);
+    if ((int64_t)blockIdx.x < P) {
+      bar_expect(bar, row_bytes);
+      bulk_g2s(buf[0], F + (int64_t)blockIdx.x * n_pad, row_bytes, bar);
     }
-    for (int b = tid; b <= NB; b += kBucketThreads) cnt[b] = 0;
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  for (int64_t p = blockIdx.x; p < P; p += gridDim.x, ++it) {
+    const int b = it & 1;
+    if (tid == 0 && p + gridDim.x < P) {  // buf[b ^ 1] was released by the previous row's last barrier
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_expect(bar + (b ^ 1), row_bytes);
+      bulk_g2s(buf[b ^ 1], F + (p + gridDim.x) * n_pad, row_bytes, bar + (b ^ 1));
+    }
+    for (int q = tid; q <= NB; q += TPB) cnt[q] = 0;
     if (tid == 0) maxb = 0;
+    bar_wait(bar + b, (it >> 1) & 1u);
+    uint32_t u[PT];
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+#pragma unroll
+    for (int i = 0; i < PT; ++i) {
+      const int e = tid + i * TPB;
+      u[i] = ord_key(buf[b][e < n ? e : 0]);
+      if (e < n) {
+        kmin = min(kmin, u[i]);
+        kmax = max(kmax, u[i]);
+      }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
@@ -288,27 +322,29 @@ __global__ void __launch_bounds__(kBucketThreads) sort_bucket_kernel(const float
       red[warp][1] = kmax;
     }
     __syncthreads();
-    kmin = min(min(red[0][0], red[1][0]), min(red[2][0], red[3][0]));
-    kmax = max(max(red[0][1], red[1][1]), max(red[2][1], red[3][1]));
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) {
+      kmin = min(kmin, red[w][0]);
+      kmax = max(kmax, red[w][1]);
+    }
     const float scale = (float)NB / ((float)(kmax - kmin) + 1.0f);
     // histogram: the atomic's return value is the key's slot inside its bucket
-    int slot[N2 / kBucketThreads], bk[N2 / kBucketThreads];
+    int slot[PT], bk[PT];
 #pragma unroll
-    for (int i = 0; i < N2 / kBucketThreads; ++i) {
-      const int e = tid + i * kBucketThreads;
+    for (int i = 0; i < PT; ++i) {
+      const int e = tid + i * TPB;
       if (e < n) {
-        const int b = min(NB - 1, (int)((float)(raw[e] - kmin) * scale));
-        bk[i] = b;
-        slot[i] = atomicAdd(&cnt[b], 1);
+        const int bb = min(NB - 1, (int)((float)(u[i] - kmin) * scale));
+        bk[i] = bb;
+        slot[i] = atomicAdd(&cnt[cidx(bb)], 1);
       }
     }
     __syncthreads();
-    // exclusive scan of the NB counters (each thread NB/128 consecutive ones), largest bucket
-    constexpr int PER = NB / kBucketThreads;
+    // exclusive scan of the NB counters (each thread NB/TPB consecutive ones), largest bucket
     int loc[PER], sum = 0, mb = 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      loc[i] = cnt[tid * PER + i];
+      loc[i] = cnt[i * TPB + tid];
       mb = max(mb, loc[i]);
       sum += loc[i];
     }
@@ -327,56 +363,57 @@ __global__ void __launch_bounds__(kBucketThreads) sort_bucket_kernel(const float
     for (int w = 0; w < warp; ++w) base += (int)red[w][0];
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      cnt[tid * PER + i] = base;
+      cnt[i * TPB + tid] = base;
       base += loc[i];
     }
-    if (tid == kBucketThreads - 1) cnt[NB] = n;
+    if (tid == TPB - 1) cnt[NB] = n;
     __syncthreads();
     const bool fallback = maxb > kMaxBucket;
     if (!fallback) {
 #pragma unroll
-      for (int i = 0; i < N2 / kBucketThreads; ++i) {
-        const int e = tid + i * kBucketThreads;
+      for (int i = 0; i < PT; ++i) {
+        const int e = tid + i * TPB;
         if (e < n) {
-          const int q = cnt[bk[i]] + slot[i];
-          key[q] = raw[e];
-          idx[q] = (uint16_t)e;
+          const int q = cnt[cidx(bk[i])] + slot[i];
+          key[q] = u[i];
         }
       }
       __syncthreads();
       // final position of each key: its bucket's start + its rank inside the bucket (smaller keys,
       // then equal keys at lower slots) -- independent per key, no sequential insertion
 #pragma unroll
-      for (int i = 0; i < N2 / kBucketThreads; ++i) {
-        const int e = tid + i * kBucketThreads;
+      for (int i = 0; i < PT; ++i) {
+        const int e = tid + i * TPB;
         if (e < n) {
-          const int lo = cnt[bk[i]], hi = cnt[bk[i] + 1], q = lo + slot[i];
-          const uint32_t kv = raw[e];
+          const int lo = cnt[cidx(bk[i])], hi = cnt[cidx(bk[i] + 1)], q = lo + slot[i];
+          const uint32_t kv = u[i];
           int rank = 0;
           for (int j = lo; j < hi; ++j) {
             const uint32_t kj = key[j];
             rank += (kj < kv || (kj == kv && j < q)) ? 1 : 0;
           }
-          sk[lo + rank] = kv;
+          sv[lo + rank] = key_float(kv);
           si[lo + rank] = (uint16_t)e;
         }
       }
     } else {
       // a stretched row: block bitonic network over N2 slots (+inf-key padding sorts last)
-      for (int e = tid; e < N2; e += kBucketThreads) {
-        key[e] = e < n ? raw[e] : 0xFFFFFFFFu;
+#pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        const int e = tid + i * TPB;
+        key[e] = e < n ? u[i] : 0xFFFFFFFFu;
         idx[e] = (uint16_t)(e < n ? e : 0xFFFF);
       }
       __syncthreads();
       for (int size = 2; size <= N2; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          for (int c = tid; c < (N2 >> 1); c += kBucketThreads) {
+          for (int c = tid; c < (N2 >> 1); c += TPB) {
             const int lo = 2 * c - (c & (stride - 1));
             const int hi = lo + stride;
             const bool asc = (lo & size) == 0;
-            const uint32_t a = key[lo], b = key[hi];
-            if ((a > b) == asc) {
-              key[lo] = b;
+            const uint32_t a = key[lo], bv = key[hi];
+            if ((a > bv) == asc) {
+              key[lo] = bv;
               key[hi] = a;
               const uint16_t t = idx[lo];
               idx[lo] = idx[hi];
@@ -386,26 +423,32 @@ __global__ void __launch_bounds__(kBucketThreads) sort_bucket_kernel(const float
           __syncthreads();
         }
       }
+      for (int e = tid; e < n; e += TPB) {
+        sv[e] = key_float(key[e]);
+        si[e] = idx[e];
+      }
+    }
+    for (int e = n + tid; e < n_pad; e += TPB) {  // pad: +inf, index 0xFFFF
+      sv[e] = INFINITY;
+      si[e] = (uint16_t)0xFFFF;
     }
     __syncthreads();
-    const uint32_t* ok_ = fallback ? key : sk;
-    const uint16_t* oi_ = fallback ? idx : si;
-    for (int e = tid; e < n_pad; e += kBucketThreads) {
-      S[p * n_pad + e] = e < n ? key_float(ok_[e]) : INFINITY;
-      perm[p * n_pad + e] = e < n ? oi_[e] : (uint16_t)0xFFFF;
-    }
-    __syncthreads();  // smem reused by the next row
+    float4* S4 = reinterpret_cast<float4*>(S + p * n_pad);
+    for (int q = tid; q < (n_pad >> 2); q += TPB) S4[q] = reinterpret_cast<const float4*>(sv)[q];
+    uint4* P8 = reinterpret_cast<uint4*>(perm + p * n_pad);
+    for (int q = tid; q < (n_pad >> 3); q += TPB) P8[q] = reinterpret_cast<const uint4*>(si)[q];
+    __syncthreads();  // smem (and buf[b]) reused by the next rows
   }
 }
 
-template <int NB, int N2>
+template <int NB, int N2, int TPB>
 cudaError_t launch_sort_bucket(corr_field* f, cudaStream_t st) {
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sort_bucket_kernel<NB, N2>, kBucketThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sort_bucket_kernel<NB, N2, TPB>, TPB, 0);
   if (occ < 1) occ = 1;
-  int64_t blocks = (int64_t)kSMs * occ * 4;
+  int64_t blocks = (int64_t)kSMs * occ;  // persistent: one wave, each CTA streams its rows
   if (blocks > f->P) blocks = f->P;
-  sort_bucket_kernel<NB, N2><<<(unsigned)blocks, kBucketThreads, 0, st>>>(f->F, f->S, f->perm, f->n, f->n_pad, f->P);
+  sort_bucket_kernel<NB, N2, TPB><<<(unsigned)blocks, TPB, 0, st>>>(f->F, f->S, f->perm, f->n, f->n_pad, f->P);
   return cudaSuccess;
 }
 
@@ -506,9 +549,18 @@ cudaError_t launch_field_ingest(corr_field* f, const float* din, cudaStream_t st
       switch (N2) {  // NB = 2 N2 buckets: about 0.5 keys per bucket, so the per-bucket sorts stay short
         case 64:
         case 128:
-        case 256: er = launch_sort_bucket<512, 256>(f, st); break;
-        case 512: er = launch_sort_bucket<1024, 512>(f, st); break;
-        case 1024: er = launch_sort_bucket<2048, 1024>(f, st); break;
+        case 256: er = launch_sort_bucket<512, 256, 128>(f, st); break;
+        case 512: er = launch_sort_bucket<1024, 512, 128>(f, st); break;
+        case 1024: {
+          static const int tpb = [] {  // A/B switch: threads per row
+            const char* v = getenv("CORR_SORT_TPB");
+            return v ? atoi(v) : 128;
+          }();
+          er = tpb == 256 ? launch_sort_bucket<2048, 1024, 256>(f, st)
+               : tpb == 64 ? launch_sort_bucket<2048, 1024, 64>(f, st)
+                           : launch_sort_bucket<2048, 1024, 128>(f, st);
+          break;
+        }
         default: break;
       }
     }
