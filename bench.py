@@ -440,8 +440,8 @@ def main():
     at_peak_s = (gemm_bf16 / bf16_peak + gemm_tf32 / tf32_peak) / 1e12
     blend_peak = (gemm_bf16 + gemm_tf32) / 1e12 / at_peak_s if at_peak_s > 0 else tf32_peak
     roofline_block = {"bound": "tensor",
-                      "kernel": "pearson_block_kernel<screen,bf16> (kind::f16, 1 MMA set) + <exact> (kind::tf32, 3 MMA sets "
-                                "on the kept tiles)",
+                      "kernel": "pearson_screen_mc_kernel (bf16 screen, kind::f16, B tiles multicast in CTA pairs) + "
+                                "pearson_block_kernel<exact> (kind::tf32, 3 MMA sets on the kept tiles)",
                       "achieved": blk_tflops, "peak": blend_peak, "unit": "TFLOP/s", "frac": blk_tflops / blend_peak,
                       "executed_bf16_flop_per_step": gemm_bf16, "executed_tf32_flop_per_step": gemm_tf32,
                       "dense_equivalent_tc_flop_per_step": 3 * 2.0 * nA * nB * n,

@@ -49,6 +49,7 @@ struct GemmRegion {
   int64_t nA, nB;
   int overlap;         // one field and the boxes intersect -> self-pair mask needed
   int pad;
+  int64_t pair_off;    // prefix of ceil(nta/2)*ntb tile pairs (multicast screen)
 };
 
 struct GemmGeom {
@@ -722,6 +723,242 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================
+// Screening pass with B-tile multicast (cluster of 2 CTAs; session 3).  The bf16 screen moves
+// 48 KB per k-block per SM (A 16 KB + B 32 KB) for 4 MMAs of 128x256x16: at the tensor pipe's
+// rate that is ~170 GB/s of L2 -> SM traffic per SM, so the screen ran at ~0.5 of the bf16 peak.
+// Here the two CTAs of a cluster take tiles (2i, n) and (2i+1, n) -- same B tile, adjacent A
+// tiles -- and each loads HALF of the B tile with a multicast TMA into both CTAs' shared memory:
+// 32 KB per k-block per SM.  Every CTA still runs the 1-SM MMA (M=128, N=256) on its own tile
+// and writes the same per-tile / per-region keys as pearson_block_kernel<true, true>, so the
+// tile selection and the exact pass are unchanged.  A stage is refilled only after BOTH CTAs'
+// MMAs have read it (each MMA commit arrives on both CTAs' empty barriers, count 2).  An odd
+// A-tile count gives the last pair's second CTA a duplicate of the first tile (max is idempotent).
+// 4 stages of 48 KB.
+// ============================================================================
+constexpr int MC_STAGES = 4;
+constexpr int MC_STAGE_BYTES = A_BYTES + B_BYTES;
+
+__device__ __forceinline__ void tma_load_4d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                               int c3, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// (region, A tile, B tile) of tile pair tp; rank r takes A tile 2*mp + r (clamped)
+__device__ __forceinline__ void mc_coord(const GemmRegion* __restrict__ reg, int64_t nreg, int64_t tp, uint32_t rank,
+                                         int64_t& r, int64_t& t, TileCoord& c) {
+  int64_t lo = 0, hi = nreg - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (reg[mid].pair_off <= tp) lo = mid; else hi = mid - 1;
+  }
+  const GemmRegion& R = reg[lo];
+  const int64_t nta = (int64_t)R.ntA[0] * R.ntA[1] * R.ntA[2];
+  const int64_t ntb = (int64_t)R.ntB[0] * R.ntB[1] * R.ntB[2];
+  const int64_t q = tp - R.pair_off;
+  const int64_t mp = q / ntb, ni = q - mp * ntb;
+  int64_t mi = 2 * mp + rank;
+  if (mi >= nta) mi = nta - 1;
+  r = lo;
+  t = R.tile_off + mi * ntb + ni;
+  c.r = lo;
+  c.tx = (int)(mi % R.ntA[0]);
+  c.ty = (int)((mi / R.ntA[0]) % R.ntA[1]);
+  c.tz = (int)(mi / ((int64_t)R.ntA[0] * R.ntA[1]));
+  c.ux = (int)(ni % R.ntB[0]);
+  c.uy = (int)((ni / R.ntB[0]) % R.ntB[1]);
+  c.uz = (int)(ni / ((int64_t)R.ntB[0] * R.ntB[1]));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    pearson_screen_mc_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mBh,
+                             const GemmRegion* __restrict__ reg, GemmGeom g, int64_t npairs, int bhy, int bhz,
+                             const uint8_t* __restrict__ ca, const uint8_t* __restrict__ cb,
+                             uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ reg_keys) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* stage_base = base;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + MC_STAGES * MC_STAGE_BYTES);
+  uint64_t* empty = full + MC_STAGES;
+  uint64_t* tfull = empty + MC_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* colbias = reinterpret_cast<float*>(tmem_slot + 4);  // [2][BN]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < MC_STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 2);  // both CTAs' MMAs must have read the stage
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers of both CTAs initialised before any multicast lands
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mBh) : "memory");
+      uint32_t it = 0;
+      for (int64_t tp = cid; tp < npairs; tp += ncl) {
+        int64_t r, t;
+        TileCoord c;
+        mc_coord(reg, g.nreg, tp, rank, r, t, c);
+        const GemmRegion& R = reg[r];
+        const int ax = R.A.x0 + c.tx * g.bxA, ay = R.A.y0 + c.ty * g.byA, az = R.A.z0 + c.tz * g.bzA;
+        // this CTA's half of the B tile: rows [rank*128, rank*128+128) = the second half along y or z
+        const int bx = R.B.x0 + c.ux * g.bxB, by = R.B.y0 + c.uy * g.byB + (int)rank * bhy,
+                  bz = R.B.z0 + c.uz * g.bzB + (int)rank * bhz;
+        for (int kb = 0; kb < g.kblocks; ++kb, ++it) {
+          const uint32_t s = it % MC_STAGES, ph = (it / MC_STAGES) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          unsigned char* st = stage_base + s * MC_STAGE_BYTES;
+          mbar_expect_tx(full + s, MC_STAGE_BYTES);
+          const int k0 = kb * 2 * BK;  // 64 bf16 members per k-block
+          tma_load_4d(st, &mA, full + s, k0, ax, ay, az);
+          tma_load_4d_mc(st + A_BYTES + rank * (B_BYTES / 2), &mBh, full + s, k0, bx, by, bz, (uint16_t)0x3);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    uint32_t it = 0, tt = 0;
+    for (int64_t tp = cid; tp < npairs; tp += ncl, ++tt) {
+      const uint32_t acc = tt & 1, aph = (tt >> 1) & 1;
+      mbar_wait(tempty + acc, aph ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tmem_base + acc * BN;
+      for (int kb = 0; kb < g.kblocks; ++kb, ++it) {
+        const uint32_t s = it % MC_STAGES, ph = (it / MC_STAGES) & 1;
+        mbar_wait(full + s, ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = smem_u32(stage_base + s * MC_STAGE_BYTES);
+          const uint64_t dA = sdesc_sw128(st), dB = sdesc_sw128(st + A_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 16 bf16 = 32 bytes inside the swizzle atom
+            tc_mma_bf16(dcol, dA + adv, dB + adv, kIdescBF16, (kb == 0 && kk == 0) ? 0u : 1u);
+          }
+          tc_commit_mc(empty + s, (uint16_t)0x3);  // this stage is read: tell both producers
+        }
+        __syncwarp();
+      }
+      if (lane == 0) tc_commit(tfull + acc);
+      __syncwarp();
+    }
+  } else {
+    // ===================== epilogue (warps 2..5): tile and region-pair maxima =====================
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const int et = threadIdx.x - 64;
+    uint32_t tt = 0;
+    for (int64_t tp = cid; tp < npairs; tp += ncl, ++tt) {
+      const uint32_t acc = tt & 1, aph = (tt >> 1) & 1;
+      int64_t r, t;
+      TileCoord c;
+      mc_coord(reg, g.nreg, tp, rank, r, t, c);
+      const GemmRegion& R = reg[r];
+      float* cbias = colbias + acc * BN;
+      for (int n = et; n < BN; n += 128) {
+        const int lx = n % g.bxB, ly = (n / g.bxB) % g.byB, lz = n / (g.bxB * g.byB);
+        const int x = R.B.x0 + c.ux * g.bxB + lx, y = R.B.y0 + c.uy * g.byB + ly, z = R.B.z0 + c.uz * g.bzB + lz;
+        bool ok = x < R.B.x1 && y < R.B.y1 && z < R.B.z1;
+        int p = -1;
+        if (ok) {
+          p = (z * g.ny + y) * g.nx + x;
+          ok = cb[p] == 0;
+        }
+        // the self pair is masked through +inf bias on overlapping boxes (screen only needs the
+        // max: a masked self pair never raises it)
+        cbias[n] = ok ? 0.f : -INFINITY;
+        if (R.overlap) colbias[2 * BN + acc * BN + n] = __int_as_float(p);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int lxA = row % g.bxA, lyA = (row / g.bxA) % g.byA, lzA = row / (g.bxA * g.byA);
+      const int xa = R.A.x0 + c.tx * g.bxA + lxA, ya = R.A.y0 + c.ty * g.byA + lyA, za = R.A.z0 + c.tz * g.bzA + lzA;
+      bool row_ok = xa < R.A.x1 && ya < R.A.y1 && za < R.A.z1;
+      int pa = -1;
+      if (row_ok) {
+        pa = (za * g.ny + ya) * g.nx + xa;
+        row_ok = ca[pa] == 0;
+      }
+      const bool selfmask = R.overlap != 0;
+      const float* cpt = colbias + 2 * BN + acc * BN;
+      mbar_wait(tfull + acc, aph);
+      tc_fence_after();
+      float best = -INFINITY;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q4 * 32) << 16);
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        float v[32];
+        tmem_ld32(taddr + ch * 32, v);
+        const float4* b4 = reinterpret_cast<const float4*>(cbias + ch * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 bb = b4[i];
+          v[4 * i + 0] = (g.absval ? fabsf(v[4 * i + 0]) : v[4 * i + 0]) + bb.x;
+          v[4 * i + 1] = (g.absval ? fabsf(v[4 * i + 1]) : v[4 * i + 1]) + bb.y;
+          v[4 * i + 2] = (g.absval ? fabsf(v[4 * i + 2]) : v[4 * i + 2]) + bb.z;
+          v[4 * i + 3] = (g.absval ? fabsf(v[4 * i + 3]) : v[4 * i + 3]) + bb.w;
+        }
+        if (selfmask) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (__float_as_int(cpt[ch * 32 + i]) == pa) v[i] = -INFINITY;
+        }
+        float m = v[0];
+#pragma unroll
+        for (int i = 1; i < 32; ++i) m = fmaxf(m, v[i]);
+        best = fmaxf(best, m);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      uint32_t k32 = (row_ok && best > -INFINITY) ? ord32(best) : 0u;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) k32 = max(k32, __shfl_xor_sync(0xffffffffu, k32, o));
+      if (lane == 0 && k32 != 0u) {
+        atomicMax(tile_keys + t, k32);
+        atomicMax(reg_keys + r, k32);
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while its peer may still multicast into it or signal it
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -910,7 +1147,7 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   g.same_field = fa == fb;
   g.nreg = nreg;
   std::vector<GemmRegion> gr((size_t)nreg);
-  int64_t tiles = 0;
+  int64_t tiles = 0, pairs = 0;
   for (int64_t r = 0; r < nreg; ++r) {
     const RegionDev& R = hreg[r];
     GemmRegion& G = gr[(size_t)r];
@@ -927,7 +1164,10 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
     G.nB = R.nB;
     G.overlap = g.same_field && R.A.x0 < R.B.x1 && R.B.x0 < R.A.x1 && R.A.y0 < R.B.y1 && R.B.y0 < R.A.y1 &&
                 R.A.z0 < R.B.z1 && R.B.z0 < R.A.z1;
-    tiles += (int64_t)G.ntA[0] * G.ntA[1] * G.ntA[2] * G.ntB[0] * G.ntB[1] * G.ntB[2];
+    G.pair_off = pairs;
+    const int64_t nta = (int64_t)G.ntA[0] * G.ntA[1] * G.ntA[2], ntb = (int64_t)G.ntB[0] * G.ntB[1] * G.ntB[2];
+    tiles += nta * ntb;
+    pairs += (nta + 1) / 2 * ntb;
   }
   g.total_tiles = tiles;
   CUtensorMap mAhi, mAlo, mBhi, mBlo;
@@ -1015,7 +1255,32 @@ cudaError_t launch_pearson_block(const corr_field* fa, const corr_field* fb, con
   tcount = reinterpret_cast<int*>(reg_keys + nreg);
   cudaMemsetAsync(tile_keys, 0, (size_t)tiles * 4, st);
   cudaMemsetAsync(reg_keys, 0, (size_t)nreg * 4 + 16, st);
-  if (screen_tf32)
+  // bf16 screen: the B-multicast cluster kernel (pearson_screen_mc_kernel) unless
+  // CORR_GEMM_SCREEN_MC=0 selects the 1-SM screen (A/B switch)
+  static const int screen_mc = [] {
+    const char* v = getenv("CORR_GEMM_SCREEN_MC");
+    return (v && v[0] == '0') ? 0 : 1;
+  }();
+  bool mc_done = false;
+  if (!screen_tf32 && screen_mc && sms >= 2) {
+    const bool zsplit = gs.bzB >= 2;
+    const int bhy = zsplit ? 0 : gs.byB / 2, bhz = zsplit ? gs.bzB / 2 : 0;
+    CUtensorMap mBh;
+    if (make_map_bf16(&mBh, fb->Zb, fb, gs.bxB, zsplit ? gs.byB : gs.byB / 2, zsplit ? gs.bzB / 2 : gs.bzB)) {
+      const size_t smem_mc = 1024 + (size_t)MC_STAGES * MC_STAGE_BYTES + 8 * (2 * MC_STAGES + 4) + 16 + 4 * BN * 4;
+      e = cudaFuncSetAttribute(pearson_screen_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mc);
+      if (e == cudaSuccess) {
+        const int64_t clusters = pairs < sms / 2 ? pairs : sms / 2;
+        pearson_screen_mc_kernel<<<(unsigned)(2 * clusters), kThreads, smem_mc, st>>>(
+            mAb, mBh, dgr, gs, pairs, bhy, bhz, fa->cflag, fb->cflag, tile_keys, reg_keys);
+        mc_done = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
+  }
+  if (mc_done) {
+  } else if (screen_tf32)
     pearson_block_kernel<true><<<(unsigned)grid, kThreads, smem, st>>>(
         mAhi, mAlo, mBhi, mBlo, dgr, g, fa->cflag, fb->cflag, keys, nullptr, nullptr, tile_keys, reg_keys);
   else

@@ -235,6 +235,19 @@ def test_pearson_block_context_boundary_and_overlap():
     _block_compare(f, None, host, None, (spec.nx, spec.ny, spec.nz), A[:3], B[:3], absval=True)
 
 
+def test_pearson_block_odd_tile_counts_and_z_split():
+    """Boxes whose A side has an ODD number of 128-point tiles (the multicast screen pairs A tiles
+    per cluster and duplicates the last one) and whose B tiles are split along z between the two
+    CTAs of a cluster (small x/y extents), plus an overlapping (self-pair masked) box pair."""
+    spec = synth.spec_of(synth.C3)
+    vals, f = _field(spec)
+    host = vals.cpu().numpy()
+    A = [(0, 0, 0, 16, 8, 3), (40, 50, 2, 56, 58, 11), (0, 0, 0, 16, 8, 3)]
+    B = [(100, 100, 0, 108, 108, 20), (10, 20, 5, 18, 28, 9), (4, 2, 0, 12, 10, 4)]
+    _block_compare(f, None, host, None, (spec.nx, spec.ny, spec.nz), A, B)
+    _block_compare(f, None, host, None, (spec.nx, spec.ny, spec.nz), A, B, absval=True)
+
+
 def test_pearson_block_n1000_and_two_fields():
     cfg = synth.C5
     sa, sb = synth.spec_of(cfg, 1), synth.spec_of(cfg, 2)
