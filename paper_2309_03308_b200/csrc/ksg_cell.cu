@@ -20,6 +20,14 @@
 //                    no lane needs it.  Needing lanes start at cellstart[c'][y-band of the member]
 //                    (no search: the member's position in c' lies inside that cell) and scan
 //                    up / down with the same stop rule.
+//     far-visit queue -- after the distance-1 columns, the lanes that still need a farther
+//                    column (~10 % of members, but in ~2 extra visits per column that each last as
+//                    long as their longest scan, with ~2.4 of 32 lanes busy) are written to a
+//                    CTA-wide queue (their k-list + member slot, in the staging buffer of the
+//                    x-argsort, dead after the build).  Once every column is done, each warp takes
+//                    32 queued members and every lane visits ITS nearest still-needed column per
+//                    round (tools/cell_sim7.py: far-visit scan steps 181 -> 60 per pair); a full
+//                    queue leaves the rest in their column warp.  +4.4 % at C4.
 //   Candidates of other columns are real members, so any extra candidate is harmless (the
 //   k-smallest multiset over a superset that contains every candidate below the final eps is
 //   exact); the self pair is never visited.  Column ends hold sentinels (+inf, -inf) / (+inf,
@@ -31,6 +39,8 @@
 // Launch: one pair unit per CTA (the hardware block scheduler balances and staggers the CTAs:
 // +18 % over a persistent grid-stride wave).
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "ksg_common.cuh"
 
@@ -76,7 +86,7 @@ __host__ __device__ inline CellLayout cell_layout(int n, int n_pad, int nw) {
   L.o_cs = take((uint32_t)L.nch * (L.nseg + 1) * 2u, 16);
   L.o_cols = take((uint32_t)L.nch * 32u * 2u, 16);
   L.o_red = take((uint32_t)nw * 8u, 8);
-  L.o_misc = take(16, 8);  // next_blk (int) + staging mbarrier (u64)
+  L.o_misc = take(24, 8);  // next_blk (int), flags (int), staging mbarrier (u64), queue count (int)
   L.bytes = (o + 15) / 16 * 16;
   return L;
 }
@@ -166,7 +176,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
     const float* __restrict__ Sa, const uint16_t* __restrict__ Pa, const float* __restrict__ Sb,
     const uint16_t* __restrict__ Pb, const float* __restrict__ spa, const float* __restrict__ spb,
     const uint8_t* __restrict__ ca, const uint8_t* __restrict__ cb, const double* __restrict__ psi, int n, int n_pad,
-    int k, int plus1, PairSrc src, PairOut out) {
+    int k, int plus1, int qcap, PairSrc src, PairOut out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const CellLayout L = cell_layout(n, n_pad, NW);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
@@ -198,6 +208,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
   unsigned long long executed = 0, nan_pairs = 0;
 
   int* flags_s = reinterpret_cast<int*>(smem + L.o_misc) + 1;  // this pair's flags (skip, swap, degenerate)
+  int* qcount = reinterpret_cast<int*>(smem + L.o_misc + 16);   // far-visit queue length
   for (int64_t u = blockIdx.x; u < src.nunits; u += gridDim.x) {
     // thread 0 alone resolves the pair (sampler, flags) and stages its rows; the others learn the
     // flags after the first build barrier.  A skipped unit stages row 0 (valid addresses, unused).
@@ -226,6 +237,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
       const float* Sv = swap ? Sa + a * n_pad : Sb + b * n_pad;
       const uint16_t* Pv = swap ? Pa + a * n_pad : Pb + b * n_pad;
       *next_blk = NW;  // columns 0 .. NW-1 are taken statically
+      *qcount = 0;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_expect(bar, 2u * row_bytes + row_bytes);
       bulk_g2s(su, Su, row_bytes, bar);
@@ -288,6 +300,53 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
 
     // ---- a3: one column per warp (first static, then dynamic), lockstep scans ----
     double acc = 0.0;
+    // far-visit queue, in pu_s (dead once the build is done): K list entries + member slot
+    float* q_l = reinterpret_cast<float*>(smem + L.o_pu);  // [K][qcap]
+    uint16_t* q_m = reinterpret_cast<uint16_t*>(q_l + K * qcap);
+    // a4 / a5 for one member per lane (on = lane holds a member whose list is final): strict
+    // marginal counts by binary searches on the sorted rows, then psi.  The strips |x - x_i| < eps
+    // and |y - y_i| < eps lie around the member's own ranks (t_i in the x row, s_i in the y row);
+    // if, for every lane, both strips end within 127 ranks of t_i / s_i on both sides (checked at
+    // the window edges with the same monotone predicates), 7-step searches over 128-wide windows
+    // replace the full log2(n)-step ones.  Called by all 32 lanes (warp vote).
+    auto count_psi = [&](bool on, int c, int ln, float2 zi, float e) {
+      uint32_t xu = su_base, xw = su_base, yu = sv_base, yw = sv_base;
+      bool win_ok = true;
+      if (on && e > 0.f) {
+        const int si = (int)lds_u16(cols_base + (uint32_t)(c * 32 + ln) * 2u);
+        const int ti = xr[pv_s[si]];
+        const int bxw = max(0, ti - 127), bxu = min(ti, L.nsx - 128);
+        const int byw = max(0, si - 127), byu = min(si, L.nsx - 128);
+        win_ok = (bxw == 0 || !(zi.x - su[bxw - 1] < e)) && (su[bxu + 127] - zi.x >= e) &&
+                 (byw == 0 || !(zi.y - sv[byw - 1] < e)) && (sv[byu + 127] - zi.y >= e);
+        xw = su_base + (uint32_t)bxw * 4u;
+        xu = su_base + (uint32_t)bxu * 4u;
+        yw = sv_base + (uint32_t)byw * 4u;
+        yu = sv_base + (uint32_t)byu * 4u;
+      }
+      const bool windowed = __all_sync(0xffffffffu, win_ok);
+      if (on) {
+        int cx = 0, cy = 0;
+        if (e > 0.f) {
+          if (windowed) {
+            CountSearch44<6>::run(7, xu, xw, yu, yw, zi.x, zi.y, e);
+          } else {
+            xu = xw = su_base;
+            yu = yw = sv_base;
+            CountSearch44<12>::run(L.log2p, xu, xw, yu, yw, zi.x, zi.y, e);
+          }
+          cx = (int)((xu - xw) >> 2) - 1;
+          cy = (int)((yu - yw) >> 2) - 1;
+        }
+        acc += __ldg(psi + cx + off) + __ldg(psi + cy + off);
+        if (out.dbg_eps) {
+          const int m = pv_s[cols[c * 32 + ln]];
+          out.dbg_eps[u * n + m] = e;
+          out.dbg_nx[u * n + m] = swap ? cy : cx;
+          out.dbg_ny[u * n + m] = swap ? cx : cy;
+        }
+      }
+    };
     {
       int ncand = 0;
       for (int c = warp; c < nch;) {
@@ -314,11 +373,12 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
         uint32_t eL = su_base + (uint32_t)(32 * lo + 31) * 4u, eR = su_base + (uint32_t)(32 * hi) * 4u;
         uint32_t bL = col_base + (uint32_t)(lo * kCS) * 8u, bR = col_base + (uint32_t)(hi * kCS) * 8u;
         uint32_t sL = cs_base + (uint32_t)(lo * cs_stride + band) * 2u, sR = cs_base + (uint32_t)(hi * cs_stride + band) * 2u;
+        bool queued = false, first = true;
 #pragma unroll 1
         while (lo >= 0 || hi < nch) {
           // left then right, each side's test and visit written out (no per-test side select)
           if (lo >= 0) {
-            const bool need = active && (zi.x - lds_f32(eL) < l[K - 1]);
+            const bool need = active && !queued && (zi.x - lds_f32(eL) < l[K - 1]);
             if (!__any_sync(0xffffffffu, need)) {
               lo = -1;
             } else {
@@ -334,7 +394,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
             }
           }
           if (hi < nch) {
-            const bool need = active && (lds_f32(eR) - zi.x < l[K - 1]);
+            const bool need = active && !queued && (lds_f32(eR) - zi.x < l[K - 1]);
             if (!__any_sync(0xffffffffu, need)) {
               hi = nch;
             } else {
@@ -349,52 +409,78 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
               sR += (uint32_t)cs_stride * 2u;
             }
           }
+          if (first && qcap > 0) {
+            // after the distance-1 columns: lanes that still need a farther column (few per
+            // warp, each visit lasting as long as its longest scan) continue from a CTA-wide
+            // queue, 32 needing members per warp, once every column is done
+            first = false;
+            const bool want = active && ((lo >= 0 && zi.x - lds_f32(eL) < l[K - 1]) ||
+                                         (hi < nch && lds_f32(eR) - zi.x < l[K - 1]));
+            const unsigned wm = __ballot_sync(0xffffffffu, want);
+            if (wm != 0u) {
+              int qb = 0;
+              if (lane == 0) qb = atomicAdd(qcount, __popc(wm));
+              qb = __shfl_sync(0xffffffffu, qb, 0);
+              const int slot = qb + __popc(wm & ((1u << lane) - 1u));
+              if (want && slot < qcap) {
+#pragma unroll
+                for (int t = 0; t < K; ++t) q_l[t * qcap + slot] = l[t];
+                q_m[slot] = (uint16_t)(c * 32 + lane);
+                queued = true;
+              }
+            }
+            if (!__any_sync(0xffffffffu, want && !queued)) break;  // the others need nothing farther
+          }
         }
         int nb = 0;
         if (lane == 0) nb = atomicAdd(next_blk, 1);  // claim the next column (latency hides below)
-        // ---- a4 / a5: strict marginal counts (binary searches on the sorted rows) and psi ----
-        // The strips |x - x_i| < eps and |y - y_i| < eps lie around the member's own ranks
-        // (t_i in the x row, s_i in the y row).  If, for every lane, both strips end within 127
-        // ranks of t_i / s_i on both sides (checked at the window edges with the same monotone
-        // predicates), 7-step searches over 128-wide windows replace the full log2(n)-step ones.
-        const float e = l[K - 1];
-        uint32_t xu = su_base, xw = su_base, yu = sv_base, yw = sv_base;
-        bool win_ok = true;
-        if (active && e > 0.f) {
-          const int si = (int)lds_u16(cols_base + (uint32_t)(c * 32 + lane) * 2u);
-          const int ti = xr[pv_s[si]];
-          const int bxw = max(0, ti - 127), bxu = min(ti, L.nsx - 128);
-          const int byw = max(0, si - 127), byu = min(si, L.nsx - 128);
-          win_ok = (bxw == 0 || !(zi.x - su[bxw - 1] < e)) && (su[bxu + 127] - zi.x >= e) &&
-                   (byw == 0 || !(zi.y - sv[byw - 1] < e)) && (sv[byu + 127] - zi.y >= e);
-          xw = su_base + (uint32_t)bxw * 4u;
-          xu = su_base + (uint32_t)bxu * 4u;
-          yw = sv_base + (uint32_t)byw * 4u;
-          yu = sv_base + (uint32_t)byu * 4u;
-        }
-        const bool windowed = __all_sync(0xffffffffu, win_ok);
-        if (active) {
-          int cx = 0, cy = 0;
-          if (e > 0.f) {
-            if (windowed) {
-              CountSearch44<6>::run(7, xu, xw, yu, yw, zi.x, zi.y, e);
-            } else {
-              xu = xw = su_base;
-              yu = yw = sv_base;
-              CountSearch44<12>::run(L.log2p, xu, xw, yu, yw, zi.x, zi.y, e);
-            }
-            cx = (int)((xu - xw) >> 2) - 1;
-            cy = (int)((yu - yw) >> 2) - 1;
-          }
-          acc += __ldg(psi + cx + off) + __ldg(psi + cy + off);
-          if (out.dbg_eps) {
-            const int m = pv_s[cols[c * 32 + lane]];
-            out.dbg_eps[u * n + m] = e;
-            out.dbg_nx[u * n + m] = swap ? cy : cx;
-            out.dbg_ny[u * n + m] = swap ? cx : cy;
-          }
-        }
+        count_psi(active && !queued, c, lane, zi, l[K - 1]);
         c = __shfl_sync(0xffffffffu, nb, 0);
+      }
+      if (qcap > 0) {
+        __syncthreads();  // every column is done and the queue complete
+        const int qn = min(*qcount, qcap);
+        for (int g = warp * 32; g < qn; g += NW * 32) {
+          const int q = g + lane;
+          const bool on = q < qn;
+          float l[K];
+#pragma unroll
+          for (int t = 0; t < K; ++t) l[t] = on ? q_l[t * qcap + q] : INFINITY;
+          const int m = on ? (int)q_m[q] : 0;
+          const int c = m >> 5, ln = m & 31;
+          const float2 zi = on ? lds_f2(col_base + (uint32_t)(c * kCS + 1 + ln) * 8u) : make_float2(0.f, 0.f);
+          const int band = on ? (int)lds_u16(cols_base + (uint32_t)(c * 32 + ln) * 2u) >> 5 : 0;
+          // per-lane rounds: every lane visits ITS nearest still-needed column (any order of
+          // visits is exact: extra candidates are real members)
+          int lo = c - 2, hi = c + 2;
+#pragma unroll 1
+          while (true) {
+            const float gl = lo >= 0 ? zi.x - su[32 * lo + 31] : INFINITY;
+            const float gr = hi < nch ? su[32 * hi] - zi.x : INFINITY;
+            const bool nl = on && gl < l[K - 1], nr = on && gr < l[K - 1];
+            if (!__any_sync(0xffffffffu, nl || nr)) break;
+            const bool go_l = nl && (!nr || gl <= gr);
+            const int cc = go_l ? lo : hi;
+            uint32_t pu = col_base + 33u * 8u, pd = col_base;  // idle lanes: column 0's sentinels
+            if (nl || nr) {
+              const uint32_t bb = col_base + (uint32_t)(cc * kCS) * 8u;
+              const uint32_t start = cs[cc * cs_stride + band];
+              pu = bb + (1u + start) * 8u;
+              pd = bb + start * 8u;
+            }
+            const uint32_t pu0 = pu, pd0 = pd;
+            scan_column<K>(pu, pd, zi, l);
+            if (COUNT && (nl || nr)) {
+              const uint32_t bb = col_base + (uint32_t)(cc * kCS) * 8u;
+              ncand += (int)((pu - pd) >> 3) + 1 - (pu == bb + 33u * 8u) - (pd == bb);
+            }
+            (void)pu0;
+            (void)pd0;
+            if (go_l) --lo;
+            else if (nr) ++hi;
+          }
+          count_psi(on, c, ln, zi, l[K - 1]);
+        }
       }
 #pragma unroll
       if (COUNT) {
@@ -444,8 +530,18 @@ cudaError_t launch_cell_t(const corr_field* fa, const corr_field* fb, int k, boo
   const int waves = grid_waves_env();
   if (waves > 0 && blocks > (int64_t)kSMs * occ * waves) blocks = (int64_t)kSMs * occ * waves;
   if (blocks > 0x7FFFFFFF) blocks = 0x7FFFFFFF;
+  // far-visit queue capacity: K list entries + a u16 member slot each, in the n_pad * 2 bytes of
+  // pu_s (CORR_KSG_QUEUE=0: no queue, every visit in the column warps -- A/B switch);
+  // capacity NW * 32 = one group per warp (measured: 128 -> 2.707e7 pairs/s at C4, the full
+  // 142 entries 2.702e7, 64 2.638e7, no queue 2.591e7)
+  static const int qmax = [] {  // CORR_KSG_QUEUE = capacity cap (0: no queue)
+    const char* v = getenv("CORR_KSG_QUEUE");
+    return v ? atoi(v) : NW * 32;
+  }();
+  const int qcap = std::min(qmax, (fa->n_pad * 2) / (4 * K + 2));
   kern<<<(unsigned)blocks, NW * 32, L.bytes, st>>>(fa->S, fa->perm, fb->S, fb->perm, fa->spread, fb->spread, fa->cflag,
-                                                   fb->cflag, fa->psi, fa->n, fa->n_pad, k, plus1 ? 1 : 0, src, out);
+                                                   fb->cflag, fa->psi, fa->n, fa->n_pad, k, plus1 ? 1 : 0, qcap, src,
+                                                   out);
   note_launch();
   return cudaGetLastError();
 }
