@@ -482,7 +482,6 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
           count_psi(on, c, ln, zi, l[K - 1]);
         }
       }
-#pragma unroll
       if (COUNT) {
         for (int o = 16; o; o >>= 1) ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
         if (lane == 0) executed += (unsigned long long)ncand;
