@@ -608,3 +608,42 @@ def test_concurrent_streams_same_field():
         assert torch.equal(got_k[0], ref_k[0]) and torch.equal(got_k[1], ref_k[1])
         assert torch.equal(got_p[0], ref_p[0]) and torch.equal(got_p[1], ref_p[1])
     f.close()
+
+
+_QUEUE_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path[:0] = [{root!r}, {tests!r}]
+import oracle
+from paper_2309_03308_b200 import binding as cb
+from paper_2309_03308_b200 import synth
+spec = synth.field_spec(8, 8, 4, 1000, seed=4242)
+vals = synth.generate(spec, device="cuda")
+f = cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members)
+a, b = synth.random_pairs(spec.points, 48, seed=7)
+a, b = a.numpy(), b.numpy()
+eps, nx, ny = cb.corr_ksg_debug(f, None, 3, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+cb.corr_check(f)
+reps, rnx, rny = oracle.knn_pairs(vals.cpu(), None, 3, a, b)
+ok = (np.array_equal(eps.cpu().numpy(), reps) and np.array_equal(nx.cpu().numpy(), rnx)
+      and np.array_equal(ny.cpu().numpy(), rny))
+print("bit-exact" if ok else "MISMATCH")
+sys.exit(0 if ok else 1)
+"""
+
+
+@pytest.mark.parametrize("qcap", ["0", "2", "128"])
+def test_ksg_far_visit_queue_capacities(qcap):
+    """The column-cell kernel's far-visit queue: no queue (every far visit in the
+    column warp), a 2-entry queue (almost every far lane overflows back into its column warp) and
+    the default capacity give bit-exact eps / counts at n = 1000.  The capacity is read once per
+    process (CORR_KSG_QUEUE), hence the subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = _QUEUE_SCRIPT.format(root=root, tests=os.path.join(root, "tests"))
+    env = dict(os.environ, CORR_KSG_QUEUE=qcap)
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "bit-exact" in r.stdout, r.stdout + r.stderr
