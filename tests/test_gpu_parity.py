@@ -647,3 +647,39 @@ def test_ksg_far_visit_queue_capacities(qcap):
     env = dict(os.environ, CORR_KSG_QUEUE=qcap)
     r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "bit-exact" in r.stdout, r.stdout + r.stderr
+
+
+_SCREEN_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path[:0] = [{root!r}]
+from paper_2309_03308_b200 import binding as cb
+from paper_2309_03308_b200 import synth
+spec = synth.spec_of(synth.C3)
+vals = synth.generate(spec, device="cuda")
+f = cb.corr_field_create(vals, spec.nx, spec.ny, spec.nz, spec.members)
+bricks = synth.bricks_of(synth.C3)
+A = [bricks[7], bricks[0], (0, 0, 0, 16, 8, 3), (100, 100, 3, 164, 110, 9)]
+B = [bricks[80], bricks[87], (4, 2, 0, 12, 10, 4), (120, 96, 0, 150, 140, 20)]
+m, a = cb.corr_region_max(f, None, cb.CORR_PEARSON, 0, A, B, 0, 0)
+np.save(sys.argv[1], np.concatenate([m.cpu().numpy().view(np.int32).astype(np.int64), a.cpu().numpy().ravel()]))
+"""
+
+
+def test_pearson_screen_multicast_equals_single_sm(tmp_path):
+    """The multicast bf16 screen (default) and the 1-SM screen (CORR_GEMM_SCREEN_MC=0) select
+    tiles from bit-identical screening values, so the exhaustive maxima and argmaxes agree bit for
+    bit (boundary, odd-tile and overlapping boxes)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = _SCREEN_SCRIPT.format(root=root)
+    outs = []
+    for mc in ("1", "0"):
+        path = str(tmp_path / f"mc{mc}.npy")
+        env = dict(os.environ, CORR_GEMM_SCREEN_MC=mc)
+        r = subprocess.run([sys.executable, "-c", script, path], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
