@@ -577,7 +577,7 @@ def main():
                 "roofline": roofline, "roofline_alu_pipe": roofline_alu, "roofline_ksg_sweep": roofline_sweep, "roofline_ksg_dense": roofline_dense, "roofline_pearson_block": roofline_block,
                 "roofline_pearson_pairs": roofline_pearson_pairs, "cpu_baseline": cpu_base, "e2e": e2e, "clocks": clk,
                 "gpu_launches": launches, "field_create_s": create_s,
-                "ingest": {"bound": "hbm", "kernels": "transpose_kernel + stats_kernel + sort_radix_kernel",
+                "ingest": {"bound": "hbm", "kernels": "transpose_kernel + stats_kernel + sort_bucket_kernel (n <= 1024; sort_radix_kernel above)",
                            "ms": ing_ms, "bytes": sum(ing_bytes.values()), "bytes_by_kernel": ing_bytes,
                            "achieved": sum(ing_bytes.values()) / (ing_ms / 1e3) / 1e9, "unit": "GB/s",
                            "peak": peaks.get("hbm_gbs") or 6552.3,
