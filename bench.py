@@ -458,7 +458,11 @@ def main():
                               "peak": peaks.get("hbm_gbs") or 6552.3, "unit": "GB/s",
                               "frac": ps_gbs / (peaks.get("hbm_gbs") or 6552.3),
                               "pairs_per_s": my_pairs / (stage_ms["pearson_sampled"] / 1e3),
-                              "ms_per_step": stage_ms["pearson_sampled"]}
+                              "ms_per_step": stage_ms["pearson_sampled"],
+                              # ncu dram__bytes of pearson_screen_kernel<16> on this workload
+                              # (profiles/r02_pearson_ncu_summary.txt: 58.15 GB read + 0.09 GB
+                              # written for the 15.68 M pairs of C4, S = 4096)
+                              "traffic_bytes_per_pair_ncu": (58.146e9 + 0.087e9) / 15679488}
 
     # e2e: same metric from HOST memory through the C ABI.  Every step passes the pinned host field
     # (7.04 GB member-major fp32) to corr_field_update, which streams it to the device itself
