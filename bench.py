@@ -532,9 +532,9 @@ def main():
             if world > 1:
                 tdist.barrier()
             torch.cuda.synchronize()
-            # at least 6 steps: the first step's update is the pipeline fill (not overlapped), later
-            # updates overlap the previous step's compute
-            ne = max(6, args.steps)
+            # at least 20 steps: the first step's update is the pipeline fill (not overlapped, and
+            # included in the time), later updates overlap the previous step's compute
+            ne = max(20, args.steps)
             e2e_clocks = ClockSampler(local)
             e2e_clocks.start()
             te = time.perf_counter()
@@ -554,7 +554,9 @@ def main():
                    "includes": "per step and rank: corr_field_update(pinned HOST pointer of the 7.04 GB field) -- "
                                "the library streams it (32-member slices, cudaMemcpyAsync on its copy stream) and "
                                "re-ingests -- then the step and the D2H of the maxima; double-buffered (the next "
-                               "field's update overlaps the current step)"}
+                               "field's update overlaps the current step); the first step's upload (pipeline fill, not "
+                               "overlapped) is inside the timed region",
+                   "steps": ne}
             slots[1].close()
             del host
 
