@@ -156,10 +156,13 @@ struct CountSearch44 {
       constexpr int ST = (1 << B) * 4;
       const float pxu = lds_imm<ST - 4>(xu), pxw = lds_imm<ST - 4>(xw);
       const float pyu = lds_imm<ST - 4>(yu), pyw = lds_imm<ST - 4>(yw);
-      xu = (pxu - x >= e) ? xu : xu + ST;
-      xw = (x - pxw < e) ? xw : xw + ST;
-      yu = (pyu - y >= e) ? yu : yu + ST;
-      yw = (y - pyw < e) ? yw : yw + ST;
+      // the x and y differences in packed pairs (sub.rn.f32x2: the same RN fp32 subtractions)
+      const float2 du = sub2(make_float2(pxu, pyu), make_float2(x, y));
+      const float2 dw = sub2(make_float2(x, y), make_float2(pxw, pyw));
+      xu = (du.x >= e) ? xu : xu + ST;
+      xw = (dw.x < e) ? xw : xw + ST;
+      yu = (du.y >= e) ? yu : yu + ST;
+      yw = (dw.y < e) ? yw : yw + ST;
     }
     CountSearch44<B - 1>::run(log2p, xu, xw, yu, yw, x, y, e);
   }
