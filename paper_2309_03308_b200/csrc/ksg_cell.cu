@@ -320,8 +320,10 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
         const int ti = xr[pv_s[si]];
         const int bxw = max(0, ti - 127), bxu = min(ti, L.nsx - 128);
         const int byw = max(0, si - 127), byu = min(si, L.nsx - 128);
-        win_ok = (bxw == 0 || !(zi.x - su[bxw - 1] < e)) && (su[bxu + 127] - zi.x >= e) &&
-                 (byw == 0 || !(zi.y - sv[byw - 1] < e)) && (sv[byu + 127] - zi.y >= e);
+        // branch-free (the four edge tests as packed differences, no short-circuit branches)
+        const float2 dl = sub2(zi, make_float2(su[max(bxw - 1, 0)], sv[max(byw - 1, 0)]));
+        const float2 dh = sub2(make_float2(su[bxu + 127], sv[byu + 127]), zi);
+        win_ok = ((bxw == 0) | !(dl.x < e)) & (dh.x >= e) & ((byw == 0) | !(dl.y < e)) & (dh.y >= e);
         xw = su_base + (uint32_t)bxw * 4u;
         xu = su_base + (uint32_t)bxu * 4u;
         yw = sv_base + (uint32_t)byw * 4u;
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
               sR += (uint32_t)cs_stride * 2u;
             }
           }
-          if (first && qcap > 0) {
+          if (qcap > 0 && __all_sync(0xffffffffu, first)) {
             // after the distance-1 columns: lanes that still need a farther column (few per
             // warp, each visit lasting as long as its longest scan) continue from a CTA-wide
             // queue, 32 needing members per warp, once every column is done
