@@ -110,6 +110,14 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
 
 __device__ __forceinline__ float chebd(float2 d) { return fmaxf(fabsf(d.x), fabsf(d.y)); }
 
+// psi table entry m (m >= 0): one 32 x 32 -> 64-bit multiply-add for the address instead of the
+// sign-extended 64-bit index arithmetic the compiler emits for psi[m + off]
+__device__ __forceinline__ double ldg_psi(const double* base, uint32_t m) {
+  const double* a;
+  asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(a) : "r"(m), "l"(base));
+  return __ldg(a);
+}
+
 // Lockstep up / down scan of one column for the whole warp, one candidate per direction per
 // step.  A direction stops once fl(y_j - y_i) >= l[K-1]; its pointer then rests on that
 // candidate, whose distance is >= l[K-1] (re-merging it is a no-op).  Column ends hold
@@ -217,6 +225,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
   const uint32_t row_bytes = (uint32_t)n_pad * 4u;
   const double psi_nk = __ldg(psi + n) + __ldg(psi + k);
   const int off = plus1 ? 1 : 0;
+  const double* __restrict__ psi_o = psi + off;  // psi(m + off), indexed by unsigned 32-bit counts
   unsigned long long executed = 0, nan_pairs = 0;
 
   int* flags_s = reinterpret_cast<int*>(smem + L.o_misc) + 1;  // this pair's flags (skip, swap, degenerate)
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 6 : 4)) ksg_cell_kernel(
           cx = (int)((xu - xw) >> 2) - 1;
           cy = (int)((yu - yw) >> 2) - 1;
         }
-        acc += __ldg(psi + cx + off) + __ldg(psi + cy + off);
+        acc += ldg_psi(psi_o, (uint32_t)cx) + ldg_psi(psi_o, (uint32_t)cy);
         if (out.dbg_eps) {
           const int m = pv_s[cols[c * 32 + ln]];
           out.dbg_eps[u * n + m] = e;
