@@ -221,7 +221,9 @@ cudaError_t launch_pearson_pairs(const corr_field* fa, const corr_field* fb, con
   if (src.nunits == 0) return cudaSuccess;
   const int nq = fa->n_pad / 4;
   int lpp = 4;
-  while (lpp < 32 && lpp * 4 < nq) lpp <<= 1;
+  // at most 8 lanes per pair (>= 4 pairs per warp, more loads in flight per lane): the Table-1
+  // one-to-all PPMCC at n = 1000 1.72 -> 1.28 ms (16 lanes: 1.47 ms)
+  while (lpp < 8 && lpp * 4 < nq) lpp <<= 1;
   static const int noscreen = [] {
     const char* v = getenv("CORR_PAIRS_NOSCREEN");  // A/B switch: every pair in fp32
     return (v && v[0] == '1') ? 1 : 0;
